@@ -1,0 +1,449 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 median-filter hot path (BASELINE.json metric).
+
+Metric: median-filter output samples/s (whole job, all ranks) and the fraction of the
+HBM roofline.  Default workload = BASELINE config 2: a float32 signal of 2^26 samples
+per GPU (SplitMix64 seed 2 uniform[0,1)) filtered at every k of the
+sweep {3, 31, 255, 1023}; one step = the whole sweep (four filter calls).  Inputs
+(268 MB per GPU) exceed the 126 MB L2, so no flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c3|c4|c5] [--impl ours|reference]
+
+N > 1 (torchrun, one rank per GPU): weak scaling.  The global signal has N * 2^26
+samples; rank g filters its contiguous output range with a (k-1)-sample halo
+(paper_1406_1717_b200.shard), generated in place on its own GPU.  No collective
+touches the data path; the timing barrier and max-over-ranks reduction are the only
+NCCL calls.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref: the
+unmodified reference headers, halo-sharded over every host core) on the same
+config/metric; under torchrun only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (dtype, n_per_gpu, ks, generator, seed, rows)
+    "c1": ("float64", 1_000_000, (101,), "uniform_f64", 1, 1),
+    "c2": ("float32", 1 << 26, (3, 31, 255, 1023), "uniform_f32", 2, 1),
+    "c3": ("int32", 65536, (255,), "mod_i32", 3, 4096),
+    "c4": ("float64", 1 << 27, (10001,), "trend_f64", 4, 1),
+    "c5": ("float32", 1 << 30, (100001,), "uniform_f32", 5, 1),
+}
+WORKLOAD = {
+    "c1": "config1: n=1e6 f64 uniform seed1, k=101",
+    "c2": "config2: n=2^26 f32 uniform seed2 per GPU, k sweep {3,31,255,1023} (one step = all four)",
+    "c3": "config3: 4096 rows x 65536 i32 uniform[0,16) seed3, k=255",
+    "c4": "config4: n=2^27 f64 i/n+N(0,0.01) seed4, k=10001",
+    "c5": "config5: n=2^30 f32 uniform seed5, k=100001",
+}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        if not self.rows:
+            return None
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_input(cfg, rank, world, k_max, device):
+    """This rank's input slice of the global signal (device resident), plus shard info."""
+    import torch
+    import paper_1406_1717_b200 as mf
+    dtype, n, ks, gen, seed, rows = CONFIGS[cfg]
+    if rows > 1:   # batched rows: shard whole rows, global row r = stream offset r*n
+        r0, r1 = mf.shard_rows(rows * world, world)[rank]
+        x = mf.generate_device(gen, seed, (r1 - r0) * n, offset=r0 * n, device=device, mod=16)
+        return x.view(r1 - r0, n)
+    n_global = n * world
+    # the union of the shards for every k: take the widest halo
+    sh = mf.shard_outputs(n_global, min(ks), world)[rank]
+    begin, end = sh.in_begin, min(n_global, sh.in_end + k_max)
+    if gen == "trend_f64":
+        full = mf.generate_trend_f64(seed, n_global)
+        return torch.from_numpy(full[begin:end]).to(f"cuda:{device}"), begin
+    return mf.generate_device(gen, seed, end - begin, offset=begin, device=device), begin
+
+
+def shard_views(cfg, x, begin, rank, world, k):
+    """(input view, n_out) of this rank's shard for window k."""
+    import paper_1406_1717_b200 as mf
+    dtype, n, ks, gen, seed, rows = CONFIGS[cfg]
+    sh = mf.shard_outputs(n * world, k, world)[rank]
+    a = sh.in_begin - begin
+    return x[a:a + sh.n_in], sh.n_out
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_1406_1717_b200 as mf
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    cfg = args.config
+    dtype, n, ks, gen, seed, rows = CONFIGS[cfg]
+    ctx = mf.Context.get(local)
+    stream = torch.cuda.Stream(device=local)
+    width = np.dtype(dtype).itemsize
+
+    with torch.cuda.stream(stream):
+        if rows > 1:
+            x = make_input(cfg, rank, world, max(ks), local)
+            jobs = [(k, x, x.shape[0] * (n - k + 1)) for k in ks]
+            outs = {k: torch.empty((x.shape[0], n - k + 1), dtype=x.dtype, device=x.device) for k in ks}
+        else:
+            x, begin = make_input(cfg, rank, world, max(ks), local)
+            jobs = []
+            outs = {}
+            for k in ks:
+                xv, n_out = shard_views(cfg, x, begin, rank, world, k)
+                jobs.append((k, xv, n_out))
+                outs[k] = torch.empty(max(n_out, 1), dtype=x.dtype, device=x.device)
+    stream.synchronize()
+
+    def call(k, xv):
+        if rows > 1:
+            mf.median_filter_rows_device(xv, k, out=outs[k], stream=stream, ctx=ctx)
+        else:
+            mf.median_filter_device(xv, k, out=outs[k], stream=stream, ctx=ctx)
+        return ctx.last_launches()
+
+    # per-k event pairs for the kernel share / roofline
+    ev = {k: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)] for k in ks}
+    for _ in range(args.warmup):
+        for k, xv, _n in jobs:
+            call(k, xv)
+    stream.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    launches = 0
+    t0.record(stream)
+    for s in range(args.steps):
+        for k, xv, _n in jobs:
+            ev[k][s][0].record(stream)
+            launches += call(k, xv)
+            ev[k][s][1].record(stream)
+    t1.record(stream)
+    stream.synchronize()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clock = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    per_k_ms = {k: statistics.mean(a.elapsed_time(b) for a, b in ev[k]) for k in ks}
+    outputs_rank = sum(nout for _k, _x, nout in jobs)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        o = torch.tensor([outputs_rank], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(o, op=dist.ReduceOp.SUM)
+        outputs_total = float(o.item())
+    else:
+        outputs_total = float(outputs_rank)
+    ms_per_step = ms / args.steps
+    value = outputs_total * args.steps / (ms / 1e3)
+
+    # roofline of the dominant kernel (largest time share of the step)
+    peak, peak_src = load_peaks()
+    kdom = max(per_k_ms, key=per_k_ms.get)
+    kk, xv, nout = [j for j in jobs if j[0] == kdom][0]
+    alg_bytes = (xv.numel() + nout) * width
+    achieved = alg_bytes / (per_k_ms[kdom] / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(f"{cfg}_k{kdom}")
+
+    # end to end through the public host API (pinned host buffers, H2D + D2H timed)
+    e2e = None
+    if rank == 0 and world == 1 and not args.no_e2e:
+        e2e = run_e2e(cfg, jobs, args, width)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(cfg, args)
+
+    if rank == 0:
+        line = {
+            "metric": "median-filter output samples/sec",
+            "value": value,
+            "unit": "samples/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": {"float32": "f32", "float64": "f64", "int32": "i32"}[dtype],
+            "data": "synthetic: SplitMix64 (generators.hpp:16-29) recipe of SURVEY.md §8(d), generated on device",
+            "config": {"workload": WORKLOAD[cfg], "n_per_gpu": n * rows, "k": list(ks),
+                       "parallelism": f"halo-sharded outputs x{world}" if rows == 1 else f"rows x{world}",
+                       "l2": "inputs exceed L2 (no flush needed)" if n * rows * width > 126e6 else
+                             "input fits L2 (warm)",
+                       "per_k_ms": {str(k): per_k_ms[k] for k in ks},
+                       "per_k_samples_per_s": {str(k): [j[2] for j in jobs if j[0] == k][0] * world / (per_k_ms[k] / 1e3)
+                                               for k in ks}},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel_k": kdom,
+                         "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clock,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(cfg, jobs, args, width):
+    """Same metric through the host-buffer C ABI (mf_median_filter / _rows): every step
+    copies the input H2D from pinned memory and the medians D2H inside the timed region."""
+    import torch
+    import paper_1406_1717_b200 as mf
+    ctx = mf.Context.get(torch.cuda.current_device())
+    hx = {}
+    hy = {}
+    for k, xv, nout in jobs:
+        hx[k] = xv.cpu().pin_memory().numpy()
+        shape = (xv.shape[0], xv.shape[1] - k + 1) if xv.dim() == 2 else (max(nout, 1),)
+        hy[k] = torch.empty(shape, dtype=xv.dtype).pin_memory().numpy()
+    import ctypes as C
+    from paper_1406_1717_b200 import _native as N
+    from paper_1406_1717_b200.filter import _DTYPES, _check
+    L = N.lib()
+
+    def one(k):
+        x, y = hx[k], hy[k]
+        if x.ndim == 2:
+            _check(L.mf_median_filter_rows(ctx.handle, _DTYPES[x.dtype], x.ctypes.data, x.shape[0], x.shape[1],
+                                           x.shape[1], k, y.ctypes.data, y.shape[1]))
+        else:
+            ylen = C.c_size_t()
+            _check(L.mf_median_filter(ctx.handle, _DTYPES[x.dtype], x.ctypes.data, x.size, k, y.ctypes.data,
+                                      y.size, C.byref(ylen)))
+    steps = max(1, min(args.steps, 5))
+    for k, _x, _n in jobs:
+        one(k)
+    t = time.perf_counter()
+    for _ in range(steps):
+        for k, _x, _n in jobs:
+            one(k)
+    dt = time.perf_counter() - t
+    outputs = sum(n for _k, _x, n in jobs)
+    return {"value": outputs * steps / dt, "unit": "samples/s",
+            "h2d_bytes_per_step": int(sum(hx[k].nbytes for k in hx)),
+            "d2h_bytes_per_step": int(sum(hy[k].nbytes for k in hy)),
+            "steps": steps, "api": "mf_median_filter (host buffers, pinned)"}
+
+
+def _ref_lib():
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import Reference, Oracle  # noqa: E402  (the checker/baseline leg only)
+    if Reference.available():
+        return Reference(), "reference"
+    return Oracle(), "port"
+
+
+def _host_input(cfg, n_sample):
+    """The config's input on the host (same bits as the device generator)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import Oracle
+    o = Oracle()
+    dtype, n, ks, gen, seed, rows = CONFIGS[cfg]
+    if gen == "uniform_f32":
+        return o.uniform_f32(seed, n_sample)
+    if gen == "uniform_f64":
+        return o.uniform_f64(seed, n_sample)
+    if gen == "mod_i32":
+        return o.mod_i32(seed, 16, n_sample)
+    return o.trend_f64(seed, n_sample)
+
+
+def _time_ref(lib, kind, cfg, x, threads):
+    from oracle_lib import keymap
+    dtype, n, ks, gen, seed, rows = CONFIGS[cfg]
+    outs = 0
+    t = time.perf_counter()
+    for k in ks:
+        if rows > 1:
+            rr = x.size // n
+            y = lib.median_filter_rows(x.reshape(rr, n), k, threads) if kind == "reference" else None
+            if y is None:
+                for r in range(rr):
+                    lib.median_filter_threads(x[r * n:(r + 1) * n].astype(np.int64), k, threads)
+            outs += rr * (n - k + 1)
+        else:
+            kx = keymap(x)
+            if kind == "reference":
+                lib.median_filter_threads(kx, k, threads)
+            else:
+                lib.median_filter_threads(kx.astype(np.int64), k, threads)
+            outs += x.size - k + 1
+    return outs, time.perf_counter() - t
+
+
+def cpu_baseline(cfg, args):
+    """The reference CPU path on this host, single core, on a bounded sample."""
+    lib, kind = _ref_lib()
+    dtype, n, ks, gen, seed, rows = CONFIGS[cfg]
+    sample = min(n * rows, args.cpu_sample)
+    if rows > 1:
+        sample = max(n, sample // n * n)
+    x = _host_input(cfg, sample)
+    outs, dt = _time_ref(lib, kind, cfg, x, 1)
+    return {"value": outs / dt, "unit": "samples/s", "cores": 1, "kind": kind,
+            "sample": f"first {sample} samples of the {cfg} signal, every k of the config, 1 thread",
+            "seconds": dt}
+
+
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return
+    lib, kind = _ref_lib()
+    cfg = args.config
+    dtype, n, ks, gen, seed, rows = CONFIGS[cfg]
+    threads = os.cpu_count() or 1
+    sample = min(n * rows, args.ref_sample)
+    if rows > 1:
+        sample = max(n, sample // n * n)
+    x = _host_input(cfg, sample)
+    for _ in range(args.warmup):
+        _time_ref(lib, kind, cfg, x, threads)
+    tot_o, tot_t = 0, 0.0
+    times = []
+    for _ in range(args.steps):
+        o, t = _time_ref(lib, kind, cfg, x, threads)
+        tot_o += o
+        tot_t += t
+        times.append(t)
+    value = tot_o / tot_t
+    line = {
+        "impl": "reference",
+        "metric": "median-filter output samples/sec",
+        "value": value,
+        "unit": "samples/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot_t / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": {"float32": "f32", "float64": "f64", "int32": "i32"}[dtype],
+        "data": "synthetic: SplitMix64 recipe of SURVEY.md §8(d), host generated",
+        "config": {"workload": WORKLOAD[cfg], "k": list(ks), "sample_samples": sample},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": kind,
+                         "sample": f"first {sample} samples of the {cfg} signal per step, every k, "
+                                   f"halo-sharded over {threads} threads"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 23)
+    ap.add_argument("--ref-sample", type=int, default=1 << 24)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

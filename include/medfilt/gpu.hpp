@@ -1,0 +1,87 @@
+// medfilt/gpu.hpp -- C++ drop-in over the C ABI (include/medfilt_gpu.h).
+//
+//   template <std::signed_integral T>
+//   std::vector<T> medfilt::gpu::median_filter(std::span<const T> x, std::size_t k);
+//
+// has exactly the reference's FilterFn<T> shape (baselines.hpp:29-30), so it registers
+// in the reference's dispatch tables (bench.hpp:51-59 lookup_filter, verify.hpp:60-70
+// filter_table, medfilt_cli.cpp:45-50 run_algorithm) under the name "gpu".  Errors are
+// rethrown as std::invalid_argument with the reference's texts (core.hpp:63-69); CUDA
+// failures throw std::runtime_error.  Float/double overloads order by IEEE totalOrder.
+#pragma once
+
+#include <concepts>
+#include <cstddef>
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../medfilt_gpu.h"
+
+namespace medfilt::gpu {
+
+namespace detail {
+
+inline void check(mf_status st) {
+  if (st == MF_OK) return;
+  if (st == MF_EMPTY_INPUT || st == MF_K_ZERO || st == MF_K_EVEN || st == MF_K_TOO_LARGE)
+    throw std::invalid_argument(mf_error_message(st));
+  throw std::runtime_error(std::string(mf_status_string(st)) + ": " + mf_error_message(st));
+}
+
+// One context per host thread (contexts are not shared across threads).
+inline mf_context* context() {
+  struct Holder {
+    mf_context* ctx = nullptr;
+    ~Holder() { mf_context_destroy(ctx); }
+  };
+  thread_local Holder holder;
+  if (!holder.ctx) check(mf_context_create(0, &holder.ctx));
+  return holder.ctx;
+}
+
+template <typename T> constexpr mf_dtype dtype_of();
+template <> constexpr mf_dtype dtype_of<std::int32_t>() { return MF_I32; }
+template <> constexpr mf_dtype dtype_of<std::int64_t>() { return MF_I64; }
+template <> constexpr mf_dtype dtype_of<float>() { return MF_F32; }
+template <> constexpr mf_dtype dtype_of<double>() { return MF_F64; }
+
+template <typename T>
+std::vector<T> run(std::span<const T> x, std::size_t k) {
+  std::size_t keep = 0;
+  check(mf_window_spec(x.size(), k, nullptr, nullptr, &keep));  // core.hpp:62-76
+  std::vector<T> y(keep);
+  if (keep == 0) return y;                                        // n < k: empty
+  std::size_t len = 0;
+  check(mf_median_filter(context(), dtype_of<T>(), x.data(), x.size(), k, y.data(), y.size(), &len));
+  y.resize(len);
+  return y;
+}
+
+}  // namespace detail
+
+/// median_filter<T> (filter.hpp:149-155) on the B200.
+template <std::signed_integral T>
+  requires(sizeof(T) == 4 || sizeof(T) == 8)
+std::vector<T> median_filter(std::span<const T> x, std::size_t k) {
+  using W = std::conditional_t<sizeof(T) == 4, std::int32_t, std::int64_t>;
+  if constexpr (std::same_as<T, W>) {
+    return detail::run<T>(x, k);
+  } else {  // e.g. long vs long long of the same width
+    auto y = detail::run<W>(std::span<const W>(reinterpret_cast<const W*>(x.data()), x.size()), k);
+    return std::vector<T>(y.begin(), y.end());
+  }
+}
+
+/// Float/double extension (the reference takes signed integers only).
+inline std::vector<float> median_filter(std::span<const float> x, std::size_t k) {
+  return detail::run<float>(x, k);
+}
+inline std::vector<double> median_filter(std::span<const double> x, std::size_t k) {
+  return detail::run<double>(x, k);
+}
+
+}  // namespace medfilt::gpu

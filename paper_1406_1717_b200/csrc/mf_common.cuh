@@ -1,0 +1,75 @@
+// mf_common.cuh -- shared device-side vocabulary of the median-filter kernels.
+//
+// Keys.  Every kernel works on unsigned "ukeys" whose unsigned order is the
+// reference's sample order (core.hpp:34-38): int32/int64 flip the sign bit; float
+// and double use the IEEE totalOrder bit map of SURVEY.md §0.1 (the signed key
+// `bits >= 0 ? bits : bits ^ 0x7FF..F`, then the sign flip).  The maps are
+// bijections, so a median is emitted by inverting the map of the selected key:
+// output bits are always the bits of an input element (bit-exact by construction).
+//
+// Padding.  The reference pads the last block with +INF sentinels
+// (filter.hpp:28-36).  Here padding is virtual: a load past n yields UKEY_MAX, and
+// because padding only ever occupies the tail of a block its (key, index) pair
+// sorts after every real UKEY_MAX element of the block -- the same place the
+// sentinel takes (core.hpp:34-47).  No kept window ever contains padding
+// (filter.hpp:76-79), so padding never reaches an output.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mf {
+
+enum DType : int { DT_I32 = 0, DT_I64 = 1, DT_F32 = 2, DT_F64 = 3 };
+
+template <int DT> struct Traits;
+template <> struct Traits<DT_I32> {
+  using T = int32_t; using U = uint32_t;
+  __host__ __device__ static __forceinline__ U enc(T v) { return (U)v ^ 0x80000000u; }
+  __host__ __device__ static __forceinline__ T dec(U u) { return (T)(u ^ 0x80000000u); }
+};
+template <> struct Traits<DT_I64> {
+  using T = int64_t; using U = uint64_t;
+  __host__ __device__ static __forceinline__ U enc(T v) { return (U)v ^ 0x8000000000000000ull; }
+  __host__ __device__ static __forceinline__ T dec(U u) { return (T)(u ^ 0x8000000000000000ull); }
+};
+template <> struct Traits<DT_F32> {
+  using T = uint32_t; using U = uint32_t;  // float carried as its bits
+  __host__ __device__ static __forceinline__ U enc(T b) { return (b & 0x80000000u) ? ~b : (b ^ 0x80000000u); }
+  __host__ __device__ static __forceinline__ T dec(U u) { return (u & 0x80000000u) ? (u ^ 0x80000000u) : ~u; }
+};
+template <> struct Traits<DT_F64> {
+  using T = uint64_t; using U = uint64_t;  // double carried as its bits
+  __host__ __device__ static __forceinline__ U enc(T b) {
+    return (b & 0x8000000000000000ull) ? ~b : (b ^ 0x8000000000000000ull);
+  }
+  __host__ __device__ static __forceinline__ T dec(U u) {
+    return (u & 0x8000000000000000ull) ? (u ^ 0x8000000000000000ull) : ~u;
+  }
+};
+
+template <typename U> struct UMax;
+template <> struct UMax<uint32_t> { static constexpr uint32_t v = 0xFFFFFFFFu; };
+template <> struct UMax<uint64_t> { static constexpr uint64_t v = 0xFFFFFFFFFFFFFFFFull; };
+
+// Problem geometry shared by every kernel.  A "signal" (row) has n samples; the
+// output has keep = n-k+1 medians.  Output o = u*k + i belongs to "unit" u: the
+// window made of block u restricted to indices >= i plus block u+1 restricted to
+// indices < i.  Unit u therefore owns the k contiguous outputs [u*k, u*k+k) and is
+// exactly the reference's block pair (A = X_u, B = X_{u+1}) of filter.hpp:83-101
+// (its step i emits y[u*k+i+1]); output u*k (i = 0) is Peek of the freshly
+// constructed block u (filter.hpp:81-82 for u = 0, and the last step of the
+// previous pair otherwise).
+struct Geom {
+  const void* x;      // rows x ld_x samples
+  void* y;            // rows x ld_y outputs
+  uint64_t n;         // samples per row
+  uint64_t ld_x, ld_y;
+  uint32_t k, h;
+  uint64_t keep;      // outputs per row = n - k + 1 (>= 1)
+  uint64_t units;     // units per row = ceil(keep / k)
+  uint32_t rows;
+};
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
+}  // namespace mf

@@ -1,0 +1,191 @@
+// mf_large.cu -- workspace planning and launch sequence of the large-k pipeline,
+// the phase-1 (piecewise_sort) entry, and the device input generators.
+#include <algorithm>
+
+#include "mf_launch.h"
+#include "mf_large.cuh"
+
+namespace mf {
+
+namespace {
+
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+LargeGeom plan(const Geom& g, uint64_t nb) {
+  LargeGeom L{};
+  L.g = g;
+  L.nb = nb;
+  L.tiles = (g.k + LTS - 1) / LTS;
+  L.nq = 2 * g.k;
+  L.nqp = (uint32_t)align_up(L.nq, 32);
+  L.tiles2 = (L.nq + LTS - 1) / LTS;
+  // Chunk length: enough chunks per unit to fill the GPU, few enough that the
+  // per-chunk selection table stays small (C * NS counters per unit).
+  uint32_t cl = 64;
+  while (cl < 1024 && (g.k + cl - 1) / cl > 256) cl *= 2;
+  while ((g.k + cl - 1) / cl > 4096) cl *= 2;  // bounds the per-CTA histogram (2C words)
+  L.CL = cl;
+  L.C = (g.k + cl - 1) / cl;
+  L.NS = (L.nq + 1023) / 1024;
+  return L;
+}
+
+template <int DT>
+struct Layout {
+  using U = typename Traits<DT>::U;
+  using E = Elem<U>;
+  size_t off_s0, off_s1, off_mk, off_org, off_rab, off_live, total;
+  Layout(const LargeGeom& L, bool sort_only) {
+    const uint64_t nel = (uint64_t)L.g.rows * L.nb * L.g.k;
+    const uint64_t nu = (uint64_t)L.g.rows * L.g.units;
+    size_t o = 0;
+    off_s0 = o; o = align_up(o + sizeof(E) * nel, 256);
+    off_s1 = o; o = align_up(o + sizeof(E) * nel, 256);
+    off_mk = off_org = off_rab = off_live = o;
+    if (!sort_only) {
+      off_mk = o; o = align_up(o + sizeof(U) * nu * L.nqp, 256);
+      off_org = o; o = align_up(o + sizeof(uint32_t) * nu * L.nqp, 256);
+      off_rab = o; o = align_up(o + sizeof(uint2) * nu * L.g.k, 256);
+      off_live = o; o = align_up(o + sizeof(uint32_t) * nu * L.C * L.NS, 256);
+    }
+    total = o;
+  }
+};
+
+// Segmented sort of every block into (key, index) order; returns the buffer holding it.
+template <int DT>
+cudaError_t sort_blocks(const LargeGeom& L, unsigned char* ws, const Layout<DT>& lay, cudaStream_t s,
+                        uint64_t* launches, Elem<typename Traits<DT>::U>** result) {
+  using E = Elem<typename Traits<DT>::U>;
+  E* bufs[2] = {reinterpret_cast<E*>(ws + lay.off_s0), reinterpret_cast<E*>(ws + lay.off_s1)};
+  dim3 grid((unsigned)(L.nb * L.tiles), L.g.rows);
+  ml_tile_sort<DT><<<grid, LT, 0, s>>>(L, bufs[0]);
+  ++*launches;
+  int cur = 0;
+  for (uint64_t run = LTS; run < L.g.k; run *= 2) {
+    ml_merge_pass<DT><<<grid, LT, 0, s>>>(L, bufs[cur], bufs[cur ^ 1], (uint32_t)run);
+    ++*launches;
+    cur ^= 1;
+  }
+  *result = bufs[cur];
+  return cudaGetLastError();
+}
+
+template <int DT>
+cudaError_t run_large_dt(const Geom& g, void* wsv, size_t ws_bytes, cudaStream_t s, uint64_t* launches) {
+  const LargeGeom L = plan(g, g.units + 1);
+  const Layout<DT> lay(L, false);
+  if (ws_bytes < lay.total) return cudaErrorMemoryAllocation;
+  unsigned char* ws = static_cast<unsigned char*>(wsv);
+  using U = typename Traits<DT>::U;
+  Elem<U>* sorted = nullptr;
+  cudaError_t e = sort_blocks<DT>(L, ws, lay, s, launches, &sorted);
+  if (e != cudaSuccess) return e;
+  U* mk = reinterpret_cast<U*>(ws + lay.off_mk);
+  uint32_t* org = reinterpret_cast<uint32_t*>(ws + lay.off_org);
+  uint2* rab = reinterpret_cast<uint2*>(ws + lay.off_rab);
+  uint32_t* live = reinterpret_cast<uint32_t*>(ws + lay.off_live);
+  const uint64_t nu = (uint64_t)g.rows * g.units;
+  ml_unit_merge<DT><<<dim3((unsigned)(g.units * L.tiles2), g.rows), LT, 0, s>>>(L, sorted, mk, org, rab);
+  ++*launches;
+  const size_t hist = sizeof(uint32_t) * 2 * L.C;
+  ml_counts<<<(unsigned)(nu * L.NS), LT, hist, s>>>(L, org, live);
+  ++*launches;
+  const uint64_t nchunks = nu * L.C;
+  ml_scan<<<(unsigned)((nchunks + LT - 1) / LT), LT, 0, s>>>(L, live, nchunks);
+  ++*launches;
+  ml_walk<DT><<<(unsigned)((nchunks + LT - 1) / LT), LT, 0, s>>>(L, mk, org, rab, live, nchunks);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+template <int DT>
+__global__ void ml_extract_perm(LargeGeom L, const Elem<typename Traits<DT>::U>* S, uint32_t* perm, uint64_t total) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < total) perm[i] = S[i].idx();
+}
+
+template <int DT>
+cudaError_t run_sort_dt(const Geom& g, uint64_t nb, void* wsv, uint32_t* perm, cudaStream_t s,
+                        uint64_t* launches) {
+  const LargeGeom L = plan(g, nb);
+  const Layout<DT> lay(L, true);
+  using U = typename Traits<DT>::U;
+  Elem<U>* sorted = nullptr;
+  cudaError_t e = sort_blocks<DT>(L, static_cast<unsigned char*>(wsv), lay, s, launches, &sorted);
+  if (e != cudaSuccess) return e;
+  const uint64_t total = (uint64_t)g.rows * nb * g.k;
+  ml_extract_perm<DT><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(L, sorted, perm, total);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+__device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t i) {
+  // value of the (i+1)-th next() of SplitMix64(seed) (generators.hpp:20-25)
+  uint64_t z = seed + (i + 1) * 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+__global__ void gen_kernel(int kind, uint64_t seed, uint64_t mod, uint64_t offset, size_t n, void* out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = splitmix_at(seed, offset + i);
+    if (kind == 0) static_cast<float*>(out)[i] = (float)((double)(r >> 40) * 0x1.0p-24);
+    else if (kind == 1) static_cast<double*>(out)[i] = (double)(r >> 11) * 0x1.0p-53;
+    else static_cast<int32_t*>(out)[i] = (int32_t)(r % mod);
+  }
+}
+
+}  // namespace
+
+size_t large_workspace_bytes(int dt, const Geom& g) {
+  const LargeGeom L = plan(g, g.units + 1);
+  switch (dt) {
+    case DT_I32: return Layout<DT_I32>(L, false).total;
+    case DT_I64: return Layout<DT_I64>(L, false).total;
+    case DT_F32: return Layout<DT_F32>(L, false).total;
+    default: return Layout<DT_F64>(L, false).total;
+  }
+}
+
+cudaError_t run_large(int dt, const Geom& g, void* ws, size_t ws_bytes, cudaStream_t s, uint64_t* launches) {
+  switch (dt) {
+    case DT_I32: return run_large_dt<DT_I32>(g, ws, ws_bytes, s, launches);
+    case DT_I64: return run_large_dt<DT_I64>(g, ws, ws_bytes, s, launches);
+    case DT_F32: return run_large_dt<DT_F32>(g, ws, ws_bytes, s, launches);
+    case DT_F64: return run_large_dt<DT_F64>(g, ws, ws_bytes, s, launches);
+  }
+  return cudaErrorInvalidValue;
+}
+
+size_t block_sort_workspace_bytes(int dt, const Geom& g, uint64_t nb) {
+  const LargeGeom L = plan(g, nb);
+  switch (dt) {
+    case DT_I32: return Layout<DT_I32>(L, true).total;
+    case DT_I64: return Layout<DT_I64>(L, true).total;
+    case DT_F32: return Layout<DT_F32>(L, true).total;
+    default: return Layout<DT_F64>(L, true).total;
+  }
+}
+
+cudaError_t run_block_sort(int dt, const Geom& g, uint64_t nb, void* ws, uint32_t* perm, cudaStream_t s,
+                           uint64_t* launches) {
+  switch (dt) {
+    case DT_I32: return run_sort_dt<DT_I32>(g, nb, ws, perm, s, launches);
+    case DT_I64: return run_sort_dt<DT_I64>(g, nb, ws, perm, s, launches);
+    case DT_F32: return run_sort_dt<DT_F32>(g, nb, ws, perm, s, launches);
+    case DT_F64: return run_sort_dt<DT_F64>(g, nb, ws, perm, s, launches);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_generate(int kind, uint64_t seed, uint64_t mod, uint64_t offset, size_t n, void* out,
+                            cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)std::min<size_t>((n + 255) / 256, 148 * 32);
+  gen_kernel<<<blocks, 256, 0, s>>>(kind, seed, mod, offset, n, out);
+  return cudaGetLastError();
+}
+
+}  // namespace mf

@@ -1,0 +1,32 @@
+// mf_launch.h -- host-side launchers shared by the translation units.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "mf_common.cuh"
+
+namespace mf {
+
+// Largest k each fused class handles (per key width).
+constexpr uint32_t kSmallMaxK = 31;
+constexpr uint32_t kMediumMaxK = 1023;
+
+// Fused small-k kernel (k odd, k <= 31).  Returns launches issued (0 on unsupported k).
+cudaError_t launch_small(int dt, const Geom& g, cudaStream_t s, uint64_t* launches);
+// Fused medium-k kernel (k <= 1023).
+cudaError_t launch_medium(int dt, const Geom& g, cudaStream_t s, uint64_t* launches);
+
+// Large-k pipeline: workspace requirement and run.
+size_t large_workspace_bytes(int dt, const Geom& g);
+cudaError_t run_large(int dt, const Geom& g, void* ws, size_t ws_bytes, cudaStream_t s, uint64_t* launches);
+// Phase-1 only (piecewise_sort): b*k permutation entries per row.
+size_t block_sort_workspace_bytes(int dt, const Geom& g, uint64_t nb);
+cudaError_t run_block_sort(int dt, const Geom& g, uint64_t nb, void* ws, uint32_t* perm, cudaStream_t s,
+                           uint64_t* launches);
+
+// Device generators.
+cudaError_t launch_generate(int kind, uint64_t seed, uint64_t mod, uint64_t offset, size_t n, void* out,
+                            cudaStream_t s);
+
+}  // namespace mf

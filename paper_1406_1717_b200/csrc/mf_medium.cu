@@ -1,0 +1,56 @@
+// mf_medium.cu -- instantiations and launcher of the fused medium-k kernel.
+#include "mf_launch.h"
+#include "mf_medium.cuh"
+
+namespace mf {
+
+namespace {
+// Warps per CTA by (R, key width): keeps the per-CTA footprint at <= ~110 KB so at
+// least two CTAs share an SM and one CTA's sort overlaps another's loads.
+template <int DT, int R> struct WarpsFor {
+  static constexpr bool wide = sizeof(typename Traits<DT>::U) == 8;
+  static constexpr int value = R >= 32 ? 2 : (R >= 16 ? (wide ? 2 : 4) : (R >= 8 ? 4 : 8));
+};
+
+template <int DT, int R>
+cudaError_t launch_r(const Geom& g, cudaStream_t s) {
+  constexpr int W = WarpsFor<DT, R>::value;
+  using C = MediumCfg<DT, R, W>;
+  auto kern = mf_medium_kernel<DT, R, W>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const uint64_t tiles = (g.units + W - 1) / W;
+  dim3 grid((unsigned)tiles, g.rows);
+  kern<<<grid, 32 * W, C::smem, s>>>(g);
+  return cudaGetLastError();
+}
+
+template <int DT>
+cudaError_t launch_dt(const Geom& g, cudaStream_t s) {
+  if (g.k <= 64) return launch_r<DT, 2>(g, s);
+  if (g.k <= 128) return launch_r<DT, 4>(g, s);
+  if (g.k <= 256) return launch_r<DT, 8>(g, s);
+  if (g.k <= 512) return launch_r<DT, 16>(g, s);
+  if (g.k <= 1024) return launch_r<DT, 32>(g, s);
+  return cudaErrorInvalidValue;
+}
+}  // namespace
+
+cudaError_t launch_medium(int dt, const Geom& g, cudaStream_t s, uint64_t* launches) {
+  cudaError_t e;
+  switch (dt) {
+    case DT_I32: e = launch_dt<DT_I32>(g, s); break;
+    case DT_I64: e = launch_dt<DT_I64>(g, s); break;
+    case DT_F32: e = launch_dt<DT_F32>(g, s); break;
+    case DT_F64: e = launch_dt<DT_F64>(g, s); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (e == cudaSuccess && launches) ++*launches;
+  return e;
+}
+
+}  // namespace mf

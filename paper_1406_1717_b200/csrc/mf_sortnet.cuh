@@ -1,0 +1,99 @@
+// mf_sortnet.cuh -- register sorting networks and the (key, index) element types.
+//
+// Phase 1 of the paper (piecewise sorting, filter.hpp:41-54) sorts (value, index)
+// pairs so that equal values keep index order (stable).  On the GPU
+// the pair is packed into one totally ordered element: for 32-bit keys a single
+// u64 (key << 32 | index), for 64-bit keys a {key, index} pair compared
+// lexicographically.  A total order makes any sorting network stable.
+//
+// The networks are Batcher odd-even merge sorts generated at compile time and
+// pruned to K inputs (the pruned comparators only touch virtual +INF slots that
+// never move in an all-ascending network), so a block of K elements sorts fully in
+// registers with every index static.
+#pragma once
+#include <cstdint>
+
+namespace mf {
+
+struct NetList {
+  int n;
+  uint8_t a[512];
+  uint8_t b[512];
+};
+
+constexpr NetList make_oem(int K) {
+  NetList net{};
+  net.n = 0;
+  int N = 1;
+  while (N < K) N <<= 1;
+  for (int p = 1; p < N; p += p)
+    for (int k = p; k > 0; k /= 2)
+      for (int j = k % p; j + k < N; j += k + k)
+        for (int i = 0; i < k && i < N - j - k; ++i)
+          if ((i + j) / (p + p) == (i + j + k) / (p + p)) {
+            const int lo = i + j, hi = i + j + k;
+            if (hi < K) {
+              net.a[net.n] = (uint8_t)lo;
+              net.b[net.n] = (uint8_t)hi;
+              ++net.n;
+            }
+          }
+  return net;
+}
+
+template <int K> struct OEM { static constexpr NetList net = make_oem(K); };
+
+// ---- element types --------------------------------------------------------------------
+template <typename U> struct Elem;
+
+template <> struct Elem<uint32_t> {
+  uint64_t v;  // key << 32 | index
+  __device__ __forceinline__ static Elem make(uint32_t key, uint32_t idx) {
+    Elem e; e.v = ((uint64_t)key << 32) | idx; return e;
+  }
+  __device__ __forceinline__ uint32_t key() const { return (uint32_t)(v >> 32); }
+  __device__ __forceinline__ uint32_t idx() const { return (uint32_t)v; }
+  __device__ __forceinline__ static bool less(const Elem& x, const Elem& y) { return x.v < y.v; }
+  __device__ __forceinline__ static void cswap(Elem& x, Elem& y) {
+    const uint64_t lo = x.v < y.v ? x.v : y.v;
+    const uint64_t hi = x.v < y.v ? y.v : x.v;
+    x.v = lo; y.v = hi;
+  }
+};
+
+template <> struct Elem<uint64_t> {
+  uint64_t k;
+  uint32_t i;
+  __device__ __forceinline__ static Elem make(uint64_t key, uint32_t idx) {
+    Elem e; e.k = key; e.i = idx; return e;
+  }
+  __device__ __forceinline__ uint64_t key() const { return k; }
+  __device__ __forceinline__ uint32_t idx() const { return i; }
+  __device__ __forceinline__ static bool less(const Elem& x, const Elem& y) {
+    return x.k < y.k || (x.k == y.k && x.i < y.i);
+  }
+  __device__ __forceinline__ static void cswap(Elem& x, Elem& y) {
+    const bool sw = less(y, x);
+    const Elem t = x;
+    x.k = sw ? y.k : x.k; x.i = sw ? y.i : x.i;
+    y.k = sw ? t.k : y.k; y.i = sw ? t.i : y.i;
+  }
+};
+
+template <int K, int I, typename E>
+__device__ __forceinline__ void net_apply(E* v) {
+  if constexpr (I < OEM<K>::net.n) {
+    constexpr int a = OEM<K>::net.a[I];
+    constexpr int b = OEM<K>::net.b[I];
+    E::cswap(v[a], v[b]);
+    net_apply<K, I + 1>(v);
+  }
+}
+
+// Sort K register-resident elements (static indices only).
+template <int K, typename E>
+__device__ __forceinline__ void sort_regs(E (&v)[K]) {
+  if constexpr (K > 1) net_apply<K, 0>(v);
+}
+
+}  // namespace mf
