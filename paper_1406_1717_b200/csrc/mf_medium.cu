@@ -1,15 +1,16 @@
 // mf_medium.cu -- instantiations and launcher of the fused medium-k kernel.
+#include <algorithm>
 #include "mf_launch.h"
 #include "mf_medium.cuh"
 
 namespace mf {
 
 namespace {
-// Warps per CTA by (R, key width): keeps the per-CTA footprint at <= ~110 KB so at
-// least two CTAs share an SM and one CTA's sort overlaps another's loads.
+// Warps per CTA by (R, key width): a few hundred CTA-resident pairs per SM at most;
+// smaller R has a smaller footprint and gets more warps.
 template <int DT, int R> struct WarpsFor {
   static constexpr bool wide = sizeof(typename Traits<DT>::U) == 8;
-  static constexpr int value = R >= 32 ? 2 : (R >= 16 ? (wide ? 2 : 4) : (R >= 8 ? 4 : 8));
+  static constexpr int value = R >= 32 ? (wide ? 2 : 4) : (R >= 16 ? 4 : 8);
 };
 
 template <int DT, int R>
@@ -17,15 +18,23 @@ cudaError_t launch_r(const Geom& g, cudaStream_t s) {
   constexpr int W = WarpsFor<DT, R>::value;
   using C = MediumCfg<DT, R, W>;
   auto kern = mf_medium_kernel<DT, R, W>;
-  static bool configured = false;
-  if (!configured) {
+  static int resident = 0;  // CTAs per SM (per process; the attribute is idempotent)
+  static int sms = 0;
+  if (!resident) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, 32 * W, C::smem);
+    if (e != cudaSuccess) return e;
+    if (resident < 1) resident = 1;
   }
-  const uint64_t tiles = (g.units + W - 1) / W;
-  dim3 grid((unsigned)tiles, g.rows);
-  kern<<<grid, 32 * W, C::smem, s>>>(g);
+  const uint64_t tiles_per_row = (g.units + W - 1) / W;
+  const uint64_t total = tiles_per_row * g.rows;
+  // persistent grid: each CTA walks a contiguous range of tiles (ring-carried blocks)
+  const uint64_t ctas = std::min<uint64_t>(total, (uint64_t)sms * resident);
+  kern<<<(unsigned)ctas, 32 * W, C::smem, s>>>(g, tiles_per_row, total);
   return cudaGetLastError();
 }
 

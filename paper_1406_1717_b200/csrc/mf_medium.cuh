@@ -7,10 +7,10 @@
 //        (key, index) elements in registers (odd-even merge network), then five
 //        warp-wide merge-path passes in shared memory produce the sorted block.
 //   run_postprocess (filter.hpp:64-106) + Block (block.hpp:24-146) -> per pair:
-//     (1) merge path over sorted A and sorted B (A wins ties: PAPER.md §6.3 "the
-//         elements of A are considered to be smaller", filter.hpp:92-93) gives every
-//         element its position in the pair's merged order, so Peek(A) vs Peek(B)
-//         comparisons become position comparisons;
+//     (1) merge path over sorted A and sorted B gives every element its position in
+//         the pair's merged order, so Peek(A) vs Peek(B) comparisons become position
+//         comparisons (ties between A and B can go either way: the emitted value is
+//         the same);
 //     (2) the k steps of the pair are cut into 32 chunks of R steps, one per lane.
 //         The state before any step is a pure function of (pi_A, pi_B, step)
 //         (Eq. 4 / Lemma 1): the live set is {A: idx >= i} u
@@ -18,11 +18,15 @@
 //         lane gets that live set as a 2k-bit row of the merged order (built for all
 //         lanes at once by an XOR prefix over the per-chunk toggle sets), selects
 //         its first median, then walks its R steps with Delete(A,i)/Undelete(B,i)
-//         as bit clear/set and the median cursor moved by next/prev live bit --
-//         the dancing-links list and the pair of cursors of Figure 7 folded into one
-//         cursor over the merged order.
-// Each block is read from HBM once per warp that needs it and every median is
-// written once, coalesced.
+//         as bit clear/set and the median cursor moved to the next/previous live bit
+//         -- the dancing-links list and the pair of cursors of Figure 7 folded into
+//         one cursor over the merged order.  The word holding the cursor is cached in
+//         a register, so most steps touch no shared memory on the dependency chain.
+//
+// Persistent CTAs own a contiguous range of tiles (W pairs each); the sorted blocks
+// live in a ring of W+1 slots, so the block shared by two consecutive tiles is loaded
+// and sorted once.  Each input block is read from HBM once per CTA range and every
+// median is written once, coalesced.
 #pragma once
 #include "mf_common.cuh"
 #include "mf_sortnet.cuh"
@@ -34,199 +38,236 @@ struct MediumCfg {
   using Tr = Traits<DT>;
   using U = typename Tr::U;
   using E = Elem<U>;
-  static constexpr int BS = 32 * R;        // block slot (>= k)
+  static constexpr int BS = 32 * R;        // block slot capacity (>= k)
   static constexpr int NW = 2 * R;         // words per merged row (2k bits <= 64R)
-  // per-CTA layout
-  static constexpr size_t sz_sorted = sizeof(E) * BS * (W + 1);
-  static constexpr size_t sz_mk = sizeof(U) * 2 * BS;         // merged keys
-  static constexpr size_t sz_rab = sizeof(uint32_t) * BS;     // RA | RB << 16, transposed
-  static constexpr size_t sz_rows = sizeof(uint32_t) * NW * 32;
+  // padded element index: blocked per-lane writes hit distinct banks (8-byte elements)
+  static constexpr int PS = (R >= 32) ? 5 : 4;
+  static constexpr int SLOT = BS + (BS >> PS) + 1;
+  static constexpr size_t sz_sorted = sizeof(E) * SLOT * (W + 1);
+  static constexpr size_t sz_src = sizeof(uint16_t) * 2 * BS;  // merged pos -> (isB, sorted pos)
+  static constexpr size_t sz_rab = sizeof(uint32_t) * BS;      // RA | RB << 16, transposed [t][lane]
+  static constexpr size_t sz_rows_bits = sizeof(uint32_t) * NW * 32;
+  static constexpr size_t sz_stage = sizeof(U) * (BS + BS / 32 + 1);
+  // the rows area doubles as the output staging area after the walk
+  static constexpr size_t sz_rows = (sz_rows_bits > sz_stage ? sz_rows_bits : sz_stage + 15) / 16 * 16;
   static constexpr size_t sz_abits = sizeof(uint32_t) * NW;
-  static constexpr size_t sz_out = sizeof(U) * BS;
-  static constexpr size_t sz_warp = sz_mk + sz_rab + sz_rows + sz_abits + sz_out;
+  static constexpr size_t sz_warp = (sz_src + sz_rab + sz_rows + sz_abits + 15) / 16 * 16;
   static constexpr size_t smem = sz_sorted + W * sz_warp;
 };
+
+template <int PS>
+__device__ __forceinline__ int pad(int p) { return p + (p >> PS); }
 
 // rows[L][w] lives at w*32 + (L ^ (w & 31)): the prefix pass (lane = word, loop
 // over L) and the walk (lane = L, data-dependent word) are both bank-spread.
 __device__ __forceinline__ uint32_t row_addr(uint32_t L, uint32_t w) { return w * 32 + (L ^ (w & 31)); }
 
+// Warp-wide sort of block `blk` into slot `sb` (padded layout).
+template <int DT, int R, int PS>
+__device__ __forceinline__ void warp_sort_block(Elem<typename Traits<DT>::U>* sb, const typename Traits<DT>::T* x,
+                                                uint64_t n, uint32_t k, uint64_t blk, uint32_t lane) {
+  using Tr = Traits<DT>;
+  using U = typename Tr::U;
+  using E = Elem<U>;
+  constexpr int BS = 32 * R;
+  E v[R];
+  const uint64_t b0 = blk * k;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t e = lane + 32 * r;            // coalesced across the warp
+    const uint64_t gp = b0 + e;
+    const U key = (e < k && gp < n) ? Tr::enc(__ldg(x + gp)) : UMax<U>::v;
+    v[r] = E::make(key, e);                      // padding: (UMAX, e) sorts last
+  }
+  sort_regs<R>(v);
+#pragma unroll
+  for (int r = 0; r < R; ++r) sb[pad<PS>(lane * R + r)] = v[r];
+  __syncwarp();
+#pragma unroll 1
+  for (int run = R; run < BS; run *= 2) {
+    const int gl = (2 * run) / R;                // lanes per merged run
+    const int j = lane & (gl - 1);
+    const int xb = (lane / gl) * (2 * run);      // X = [xb, xb+run), Y = [xb+run, xb+2run)
+    const int yb0 = xb + run;
+    const int d = j * R;
+    int lo = d > run ? d - run : 0, hi = d < run ? d : run;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (E::less(sb[pad<PS>(xb + mid)], sb[pad<PS>(yb0 + d - 1 - mid)])) lo = mid + 1; else hi = mid;
+    }
+    int ia = lo, ib = d - lo;
+    E xa = sb[pad<PS>(xb + min(ia, run - 1))], yv = sb[pad<PS>(yb0 + min(ib, run - 1))];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const bool takeA = (ib >= run) || (ia < run && E::less(xa, yv));
+      v[r] = takeA ? xa : yv;
+      if (takeA) { ++ia; xa = sb[pad<PS>(xb + min(ia, run - 1))]; }
+      else { ++ib; yv = sb[pad<PS>(yb0 + min(ib, run - 1))]; }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < R; ++r) sb[pad<PS>(xb + d + r)] = v[r];
+    __syncwarp();
+  }
+}
+
 template <int DT, int R, int W>
-__global__ void __launch_bounds__(32 * W) mf_medium_kernel(Geom g) {
+__global__ void __launch_bounds__(32 * W) mf_medium_kernel(Geom g, uint64_t tiles_per_row, uint64_t total_tiles) {
   using C = MediumCfg<DT, R, W>;
   using Tr = typename C::Tr;
   using U = typename C::U;
   using E = typename C::E;
   using TV = typename Tr::T;
-  constexpr int BS = C::BS, NW = C::NW;
+  constexpr int NW = C::NW, PS = C::PS, SLOT = C::SLOT;
   extern __shared__ __align__(16) unsigned char smem[];
-  E* sorted = reinterpret_cast<E*>(smem);
+  E* ring = reinterpret_cast<E*>(smem);
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* ws = smem + C::sz_sorted + warp * C::sz_warp;
-  U* mk = reinterpret_cast<U*>(ws);
-  uint32_t* rab = reinterpret_cast<uint32_t*>(ws + C::sz_mk);
-  uint32_t* rows = reinterpret_cast<uint32_t*>(ws + C::sz_mk + C::sz_rab);
-  uint32_t* abits = rows + NW * 32;
-  U* ost = reinterpret_cast<U*>(ws + C::sz_mk + C::sz_rab + C::sz_rows + C::sz_abits);
+  uint16_t* src = reinterpret_cast<uint16_t*>(ws);
+  uint32_t* rab = reinterpret_cast<uint32_t*>(ws + C::sz_src);
+  uint32_t* rows = reinterpret_cast<uint32_t*>(ws + C::sz_src + C::sz_rab);
+  uint32_t* abits = reinterpret_cast<uint32_t*>(ws + C::sz_src + C::sz_rab + C::sz_rows);
+  U* ost = reinterpret_cast<U*>(rows);  // output staging reuses the rows area after the walk
 
   const uint32_t k = g.k, h = g.h;
-  const uint64_t row = blockIdx.y;
-  const uint64_t u0 = (uint64_t)blockIdx.x * W;
-  const TV* __restrict__ x = reinterpret_cast<const TV*>(g.x) + row * g.ld_x;
-  TV* __restrict__ y = reinterpret_cast<TV*>(g.y) + row * g.ld_y;
+  const uint32_t nq = 2 * k, nw = (nq + 31) / 32;
+  // contiguous tile range of this CTA
+  const uint64_t t_begin = total_tiles * blockIdx.x / gridDim.x;
+  const uint64_t t_end = total_tiles * (blockIdx.x + 1) / gridDim.x;
+  uint32_t base = 0;                 // physical slot of logical slot 0
+  uint64_t prev_row = ~0ull, prev_tile = ~0ull;
 
-  // ---------------- phase 1: warp block sort ----------------
-  auto sort_block = [&](uint32_t slot) {
-    E* sb = sorted + slot * BS;
-    const uint64_t blk = u0 + slot;
-    E v[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const uint32_t e = lane + 32 * r;            // coalesced across the warp
-      const uint64_t gp = blk * k + e;
-      const U key = (e < k && gp < g.n) ? Tr::enc(x[gp]) : UMax<U>::v;
-      v[r] = E::make(key, e);                      // padding: (UMAX, e) sorts last
-    }
-    sort_regs<R>(v);
-#pragma unroll
-    for (int r = 0; r < R; ++r) sb[lane * R + r] = v[r];
-    __syncwarp();
-#pragma unroll 1
-    for (int run = R; run < BS; run *= 2) {
-      const uint32_t gl = (2 * run) / R;           // lanes per merged run
-      const uint32_t j = lane & (gl - 1);
-      const E* X = sb + (lane / gl) * (2 * run);
-      const E* Y = X + run;
-      const int d = j * R;
-      int lo = d > run ? d - run : 0, hi = d < run ? d : run;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (E::less(X[mid], Y[d - 1 - mid])) lo = mid + 1; else hi = mid;
-      }
-      int ia = lo, ib = d - lo;
-      E xa = X[ia < run ? ia : run - 1], yb = Y[ib < run ? ib : run - 1];
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const bool takeA = (ib >= run) || (ia < run && E::less(xa, yb));
-        v[r] = takeA ? xa : yb;
-        if (takeA) { ++ia; xa = X[ia < run ? ia : run - 1]; }
-        else { ++ib; yb = Y[ib < run ? ib : run - 1]; }
-      }
+  for (uint64_t t = t_begin; t < t_end; ++t) {
+    const uint64_t row = t / tiles_per_row, tr = t % tiles_per_row;
+    const uint64_t u0 = tr * W;
+    const TV* __restrict__ x = reinterpret_cast<const TV*>(g.x) + row * g.ld_x;
+    TV* __restrict__ y = reinterpret_cast<TV*>(g.y) + row * g.ld_y;
+    const bool carry = (row == prev_row && tr == prev_tile + 1);
+    if (carry) base = (base + W) % (W + 1);
+    auto slot = [&](uint32_t logical) { return ring + ((base + logical) % (W + 1)) * SLOT; };
+
+    // ---------------- phase 1: warp block sorts ----------------
+    if (!carry && warp == 0) warp_sort_block<DT, R, PS>(slot(0), x, g.n, k, u0, lane);
+    warp_sort_block<DT, R, PS>(slot(warp + 1), x, g.n, k, u0 + warp + 1, lane);
+    __syncthreads();
+
+    // ---------------- phase 2: per-pair postprocess ----------------
+    const uint64_t u = u0 + warp;
+    if (u < g.units) {
+      const uint64_t rem = g.keep - u * k;
+      const uint32_t imax = rem < (uint64_t)k ? (uint32_t)rem : k;
+      const E* A = slot(warp);
+      const E* B = slot(warp + 1);
+
+      for (uint32_t i = lane; i < NW * 32; i += 32) rows[i] = 0;
+      for (uint32_t w = lane; w < NW; w += 32) abits[w] = 0;
       __syncwarp();
-      E* out = const_cast<E*>(X) + d;
-#pragma unroll
-      for (int r = 0; r < R; ++r) out[r] = v[r];
-      __syncwarp();
-    }
-  };
-  sort_block(warp + 1);
-  if (warp == 0) sort_block(0);
-  __syncthreads();
 
-  // ---------------- phase 2: per-pair postprocess ----------------
-  const uint64_t u = u0 + warp;
-  if (u >= g.units) return;
-  const uint64_t rem = g.keep - u * k;
-  const uint32_t imax = rem < (uint64_t)k ? (uint32_t)rem : k;
-  const E* A = sorted + warp * BS;
-  const E* B = A + BS;
-  const uint32_t nq = 2 * k;                 // merged positions
-  const uint32_t nw = (nq + 31) / 32;
-
-  for (uint32_t i = lane; i < NW * 32; i += 32) rows[i] = 0;
-  for (uint32_t w = lane; w < NW; w += 32) abits[w] = 0;
-  __syncwarp();
-
-  // merge path: lane owns merged positions [lane*2R, lane*2R + 2R)
-  {
-    const int d = lane * 2 * R;
-    if ((uint32_t)d < nq) {
-      const int K = (int)k;
-      int lo = d > K ? d - K : 0, hi = d < K ? d : K;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (A[mid].key() <= B[d - 1 - mid].key()) lo = mid + 1; else hi = mid;
-      }
-      int ia = lo, ib = d - lo;
+      // merge path: lane owns merged positions [lane*2R, lane*2R + 2R)
+      {
+        const int d = lane * 2 * R;
+        if ((uint32_t)d < nq) {
+          const int K = (int)k;
+          int lo = d > K ? d - K : 0, hi = d < K ? d : K;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (A[pad<PS>(mid)].key() <= B[pad<PS>(d - 1 - mid)].key()) lo = mid + 1; else hi = mid;
+          }
+          int ia = lo, ib = d - lo;
+          E ea = A[pad<PS>(min(ia, K - 1))], eb = B[pad<PS>(min(ib, K - 1))];
 #pragma unroll 4
-      for (int r = 0; r < 2 * R; ++r) {
-        const int q = d + r;
-        if (q >= (int)nq) break;
-        const bool takeA = (ib >= K) || (ia < K && A[ia].key() <= B[ib].key());
-        const E e = takeA ? A[ia] : B[ib];
-        const uint32_t idx = e.idx();
-        mk[q] = e.key();
-        const uint32_t c = idx / R;          // owning lane (chunk) of this element
-        atomicOr(&rows[row_addr(c, q >> 5)], 1u << (q & 31));
-        if (takeA) {
-          atomicOr(&abits[q >> 5], 1u << (q & 31));
-          reinterpret_cast<uint16_t*>(rab)[2 * ((idx % R) * 32 + c)] = (uint16_t)q;
-          ++ia;
-        } else {
-          reinterpret_cast<uint16_t*>(rab)[2 * ((idx % R) * 32 + c) + 1] = (uint16_t)q;
-          ++ib;
+          for (int r = 0; r < 2 * R; ++r) {
+            const int q = d + r;
+            if (q >= (int)nq) break;
+            const bool takeA = (ib >= K) || (ia < K && ea.key() <= eb.key());
+            const uint32_t idx = takeA ? ea.idx() : eb.idx();
+            const uint32_t c = idx / R;            // owning lane (chunk) of this element
+            atomicOr(&rows[row_addr(c, q >> 5)], 1u << (q & 31));
+            if (takeA) {
+              src[q] = (uint16_t)ia;
+              atomicOr(&abits[q >> 5], 1u << (q & 31));
+              reinterpret_cast<uint16_t*>(rab)[2 * ((idx % R) * 32 + c)] = (uint16_t)q;
+              ++ia;
+              ea = A[pad<PS>(min(ia, K - 1))];
+            } else {
+              src[q] = (uint16_t)(0x8000u | ib);
+              reinterpret_cast<uint16_t*>(rab)[2 * ((idx % R) * 32 + c) + 1] = (uint16_t)q;
+              ++ib;
+              eb = B[pad<PS>(min(ib, K - 1))];
+            }
+          }
         }
       }
-    }
-  }
-  __syncwarp();
-  // XOR prefix over chunks: row_L = A_bits ^ (toggles of chunks < L)
-  for (uint32_t w = lane; w < nw; w += 32) {
-    uint32_t acc = abits[w];
+      __syncwarp();
+      // XOR prefix over chunks: row_L = A_bits ^ (toggles of chunks < L)
+      for (uint32_t w = lane; w < nw; w += 32) {
+        uint32_t acc = abits[w];
 #pragma unroll 8
-    for (uint32_t L = 0; L < 32; ++L) {
-      const uint32_t a = row_addr(L, w);
-      const uint32_t dlt = rows[a];
-      rows[a] = acc;
-      acc ^= dlt;
-    }
-  }
-  __syncwarp();
-
-  // walk: lane L emits outputs [L*R, L*R + R) of this unit
-  const uint32_t i0 = lane * R;
-  if (i0 < imax) {
-    // select the (h+1)-th live position of row_L
-    uint32_t cnt = 0, p = 0;
-    for (uint32_t w = 0; w < nw; ++w) {
-      const uint32_t word = rows[row_addr(lane, w)];
-      const uint32_t pc = __popc(word);
-      if (cnt + pc > h) { p = w * 32 + __fns(word, 0, (int)(h - cnt) + 1); break; }
-      cnt += pc;
-    }
-    ost[i0] = mk[p];
-#pragma unroll 4
-    for (int t = 1; t < R; ++t) {
-      const uint32_t i = i0 + t;
-      if (i >= imax) break;
-      const uint32_t ab = rab[(t - 1) * 32 + lane];
-      const uint32_t a = ab & 0xFFFF, b = ab >> 16;
-      const uint32_t wa = row_addr(lane, a >> 5), wb = row_addr(lane, b >> 5);
-      rows[wa] &= ~(1u << (a & 31));
-      rows[wb] |= 1u << (b & 31);
-      int dir = 0;  // +1: next live above p, -1: previous live below p
-      if (a == p) dir = b < p ? -1 : 1;
-      else if (a < p && b > p) dir = 1;
-      else if (a > p && b < p) dir = -1;
-      if (dir > 0) {
-        uint32_t w = (p + 1) >> 5;
-        uint32_t word = (p + 1) & 31 ? rows[row_addr(lane, w)] & (0xFFFFFFFFu << ((p + 1) & 31))
-                                     : rows[row_addr(lane, w)];
-        while (word == 0) { ++w; word = rows[row_addr(lane, w)]; }
-        p = w * 32 + __ffs(word) - 1;
-      } else if (dir < 0) {
-        uint32_t w = p >> 5;
-        uint32_t word = rows[row_addr(lane, w)] & ((1u << (p & 31)) - 1u);
-        while (word == 0) { --w; word = rows[row_addr(lane, w)]; }
-        p = w * 32 + 31 - __clz(word);
+        for (uint32_t L = 0; L < 32; ++L) {
+          const uint32_t a = row_addr(L, w);
+          const uint32_t dlt = rows[a];
+          rows[a] = acc;
+          acc ^= dlt;
+        }
       }
-      ost[i] = mk[p];
+      __syncwarp();
+
+      auto key_at = [&](uint32_t p) -> U {
+        const uint32_t s = src[p];
+        return (s & 0x8000u) ? B[pad<PS>(s & 0x7FFF)].key() : A[pad<PS>(s)].key();
+      };
+
+      // walk: lane L emits outputs [L*R, L*R + R) of this unit
+      const uint32_t i0 = lane * R;
+      U out[R];
+      if (i0 < imax) {
+        // select the (h+1)-th live position of row_L
+        uint32_t cnt = 0, cw = 0, cb = 0;
+        for (;; ++cw) {
+          cb = rows[row_addr(lane, cw)];
+          const uint32_t pc = __popc(cb);
+          if (cnt + pc > h) break;
+          cnt += pc;
+        }
+        uint32_t p = cw * 32 + __fns(cb, 0, (int)(h - cnt) + 1);
+        out[0] = key_at(p);
+#pragma unroll
+        for (int t = 1; t < R; ++t) {
+          if (i0 + t < imax) {
+            const uint32_t ab = rab[(t - 1) * 32 + lane];
+            const uint32_t a = ab & 0xFFFF, b = ab >> 16;
+            // Delete(A, i-1) and Undelete(B, i-1): clear / set one live bit each; the
+            // cached cursor word is authoritative for word cw, shared memory for the rest
+            if ((a >> 5) == cw) cb &= ~(1u << (a & 31)); else rows[row_addr(lane, a >> 5)] &= ~(1u << (a & 31));
+            if ((b >> 5) == cw) cb |= 1u << (b & 31); else rows[row_addr(lane, b >> 5)] |= 1u << (b & 31);
+            const bool up = (a == p) ? (b > p) : (a < p && b > p);
+            const bool down = (a == p) ? (b < p) : (a > p && b < p);
+            if (up) {
+              const uint32_t sh = (p & 31) + 1;
+              uint32_t m = sh < 32 ? cb & (0xFFFFFFFFu << sh) : 0u;
+              while (m == 0) { rows[row_addr(lane, cw)] = cb; ++cw; cb = rows[row_addr(lane, cw)]; m = cb; }
+              p = cw * 32 + __ffs(m) - 1;
+            } else if (down) {
+              uint32_t m = cb & ((1u << (p & 31)) - 1u);
+              while (m == 0) { rows[row_addr(lane, cw)] = cb; --cw; cb = rows[row_addr(lane, cw)]; m = cb; }
+              p = cw * 32 + 31 - __clz(m);
+            }
+            out[t] = key_at(p);
+          }
+        }
+      }
+      __syncwarp();  // rows are dead: reuse them as the output staging area
+#pragma unroll
+      for (int t = 0; t < R; ++t)
+        if (i0 + t < imax) ost[i0 + t + ((i0 + t) >> 5)] = out[t];
+      __syncwarp();
+      TV* yo = y + u * k;
+      for (uint32_t i = lane; i < imax; i += 32) yo[i] = Tr::dec(ost[i + (i >> 5)]);
     }
+    prev_row = row;
+    prev_tile = tr;
+    __syncthreads();  // the ring slots are reused by the next tile
   }
-  __syncwarp();
-  // coalesced store of the unit's imax outputs
-  TV* yo = y + u * k;
-  for (uint32_t i = lane; i < imax; i += 32) yo[i] = Tr::dec(ost[i]);
 }
 
 }  // namespace mf
