@@ -1,4 +1,6 @@
 // mf_small.cu -- instantiations and launcher of the fused small-k kernel.
+#include <algorithm>
+
 #include "mf_launch.h"
 #include "mf_small.cuh"
 
@@ -11,15 +13,23 @@ template <int DT, int K>
 cudaError_t launch_k(const Geom& g, cudaStream_t s) {
   using C = SmallCfg<DT, K, kSmallThreads>;
   auto kern = mf_small_kernel<DT, K, kSmallThreads>;
-  static bool configured = false;  // per-process attribute, idempotent
-  if (!configured) {
+  static int resident = 0;  // CTAs per SM (per process; the attribute is idempotent)
+  static int sms = 0;
+  if (!resident) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, kSmallThreads, C::smem);
+    if (e != cudaSuccess) return e;
+    if (resident < 1) resident = 1;
   }
-  const uint64_t tiles = (g.units + kSmallThreads - 1) / kSmallThreads;
-  dim3 grid((unsigned)tiles, g.rows);
-  kern<<<grid, kSmallThreads, C::smem, s>>>(g);
+  const uint64_t tiles_per_row = (g.units + C::TU - 1) / C::TU;
+  const uint64_t total = tiles_per_row * g.rows;
+  // persistent grid: each CTA streams a contiguous range of tiles with a prefetch
+  const uint64_t ctas = std::min<uint64_t>(total, (uint64_t)sms * resident);
+  kern<<<(unsigned)ctas, kSmallThreads, C::smem, s>>>(g, tiles_per_row, total);
   return cudaGetLastError();
 }
 

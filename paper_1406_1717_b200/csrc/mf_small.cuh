@@ -12,148 +12,222 @@
 // positions, so prev[m]/next[m] are "highest live bit below m" / "lowest live bit
 // above m" (one clz/ffs each), and the stale-link undelete of dancing links is a
 // plain bit set.  Cursor m and small-count s follow block.hpp:71-104 step for step,
-// so the per-step (m, s) state is identical to the reference's (tests pin it).
+// so the per-step (m, s) state is identical to the reference's.  Every step is
+// evaluated branch-free (selects, no divergence), fully unrolled over the K steps.
 //
-// Tile: T threads own T consecutive units (block pairs); the T+1 blocks of the
-// tile are loaded once (coalesced), sorted into a lane-interleaved smem layout
-// ([position][column], column stride a multiple of 32: every warp access is
-// conflict-free regardless of the data-dependent position), walked, staged and
-// stored coalesced.
+// Persistent CTAs stream tiles of T consecutive units: while a tile is sorted and
+// walked, the next tile's T+1 blocks are already in flight into the other half of a
+// double buffer (cp.async, 16-byte chunks), so HBM reads overlap the compute.  The
+// sorted keys and ranks use a lane-interleaved [position][column] layout whose column
+// stride is a multiple of 32, so every warp access is conflict-free regardless of
+// the data-dependent cursor positions.
 #pragma once
 #include "mf_common.cuh"
 #include "mf_sortnet.cuh"
 
 namespace mf {
 
+template <int K> struct UnitsPerThread { static constexpr int value = K <= 7 ? 4 : (K <= 15 ? 2 : 1); };
+
 template <int DT, int K, int T>
 struct SmallCfg {
   using Tr = Traits<DT>;
   using U = typename Tr::U;
   static constexpr int H = (K - 1) / 2;
-  static constexpr int SC = T + 32;  // column stride: >= T+1 and a multiple of 32
-  static constexpr size_t off_key = 0;                                   // U[K*SC]
-  static constexpr size_t off_rank = off_key + sizeof(U) * K * SC;       // u8[K*SC]
-  static constexpr size_t off_io = (off_rank + K * SC + 15) / 16 * 16;   // U[(T+1)*K]
-  static constexpr size_t smem = off_io + sizeof(U) * (T + 1) * K;
+  static constexpr int UPT = UnitsPerThread<K>::value;  // units (block pairs) per thread per tile
+  static constexpr int TU = T * UPT;                    // units per tile
+  static constexpr int NB = TU + 1;                     // blocks (columns) per tile
+  static constexpr int SC = TU + 32;                    // column stride: >= NB, a multiple of 32
+  // one input buffer (bytes): NB*K elements plus up to 16 bytes of alignment shift
+  static constexpr int IO = (NB * K * (int)sizeof(U) + 15) / 16 * 16 + 16;
+  static constexpr size_t off_key = 0;                                          // U[K*SC]
+  static constexpr size_t off_rank = off_key + sizeof(U) * K * SC;              // u8[K*SC]
+  static constexpr size_t off_io = (off_rank + K * SC + 15) / 16 * 16;          // 2 x IO bytes
+  static constexpr size_t smem = off_io + 2 * (size_t)IO;
 };
 
-// below/above helpers over a K-bit live mask (K <= 31)
-__device__ __forceinline__ uint32_t live_next(uint32_t mask, uint32_t r, uint32_t K) {
-  // lowest live position > r (r < K), or K
-  const uint32_t hi = mask >> (r + 1);
-  return hi ? r + 1 + (uint32_t)__ffs(hi) - 1 : K;
+// Forced select (selp): both operands are computed, so no divergent branch is emitted.
+__device__ __forceinline__ uint32_t sel(bool c, uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\tselp.b32 %0, %2, %3, p;\n\t}"
+      : "=r"(r) : "r"((uint32_t)c), "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t sel(bool c, uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\tselp.b64 %0, %2, %3, p;\n\t}"
+      : "=l"(r) : "r"((uint32_t)c), "l"(a), "l"(b));
+  return r;
+}
+
+// Live masks carry a sentinel bit at position K (the reference's list node k,
+// block.hpp:21-24), so "next live" always exists and needs no branch.
+__device__ __forceinline__ uint32_t live_next(uint32_t mask, uint32_t r) {
+  // lowest live position > r (r < K): the sentinel K when none
+  return r + (uint32_t)__ffs(mask >> (r + 1));
 }
 __device__ __forceinline__ uint32_t live_prev(uint32_t mask, uint32_t m, uint32_t K) {
-  // highest live position < m (m <= K), or K (the list head/tail node)
+  // highest live position < m (m <= K <= 31), or K (the list head/tail node)
   const uint32_t lo = mask & ((1u << m) - 1u);
-  return lo ? 31u - (uint32_t)__clz(lo) : K;
+  return sel(lo != 0, 31u - (uint32_t)__clz(lo), K);
 }
-__device__ __forceinline__ uint32_t live_first(uint32_t mask, uint32_t K) {
-  return mask ? (uint32_t)__ffs(mask) - 1 : K;
+__device__ __forceinline__ uint32_t live_succ(uint32_t mask, uint32_t m, uint32_t K) {
+  // next[m] of the reference list: lowest live > m, or the list head when m = k
+  const uint32_t nx = live_next(mask, m < K ? m : K - 1);
+  return sel(m == K, (uint32_t)__ffs(mask) - 1, nx);
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// Element e of a staged tile sits at buf[e + misalign(x + base)], so smem and global
+// addresses agree modulo 16 bytes and whole chunks can move with cp.async.
+template <typename TV>
+__device__ __forceinline__ int misalign(const TV* p) {
+  return (int)((reinterpret_cast<uintptr_t>(p) & 15) / sizeof(TV));
+}
+
+// Stage NE elements (raw input bits from x + base) into `buf`.  Whole 16-byte chunks
+// inside [0, n) go through cp.async; the ragged head/tail and the padding past n (the
+// reference's +INF sentinels, filter.hpp:28-36) are written directly.  The padding value
+// 0x7FF..F maps to the all-ones ukey for every dtype.
+template <typename TV, int NE, int T>
+__device__ __forceinline__ void stage_tile(TV* buf, const TV* x, uint64_t n, uint64_t base) {
+  constexpr int EPC = 16 / (int)sizeof(TV);  // elements per 16-byte chunk
+  const TV pad = (TV)(~(TV)0 >> 1);
+  const int mis = misalign(x + base);
+  TV* dst = buf + mis;
+  const TV* src = x + base;
+  const int real = n > base ? (int)(n - base < (uint64_t)NE ? n - base : (uint64_t)NE) : 0;
+  const int h0 = min((EPC - mis) % EPC, real);   // unaligned head elements
+  const int nchunks = (real - h0) / EPC;
+  const int tail0 = h0 + nchunks * EPC;
+  for (int c = threadIdx.x; c < nchunks; c += T) cp_async16(dst + h0 + c * EPC, src + h0 + c * EPC);
+  if ((int)threadIdx.x < h0) dst[threadIdx.x] = src[threadIdx.x];
+  for (int e = tail0 + threadIdx.x; e < NE; e += T) dst[e] = e < real ? src[e] : pad;
+  cp_async_commit();
 }
 
 template <int DT, int K, int T>
-__global__ void __launch_bounds__(T) mf_small_kernel(Geom g) {
+__global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_row, uint64_t total_tiles) {
   using C = SmallCfg<DT, K, T>;
   using Tr = typename C::Tr;
   using U = typename C::U;
   using TV = typename Tr::T;
   using E = Elem<U>;
-  constexpr int H = C::H, SC = C::SC;
+  constexpr int H = C::H, SC = C::SC, UPT = C::UPT, TU = C::TU, NB = C::NB;
   extern __shared__ __align__(16) unsigned char smem[];
   U* skey = reinterpret_cast<U*>(smem + C::off_key);
   uint8_t* srank = smem + C::off_rank;
-  U* io = reinterpret_cast<U*>(smem + C::off_io);
+  auto io = [&](int which) { return reinterpret_cast<TV*>(smem + C::off_io + which * C::IO); };
 
   const uint32_t t = threadIdx.x;
-  const uint64_t row = blockIdx.y;
-  const uint64_t u0 = (uint64_t)blockIdx.x * T;
-  const TV* __restrict__ x = reinterpret_cast<const TV*>(g.x) + row * g.ld_x;
-  TV* __restrict__ y = reinterpret_cast<TV*>(g.y) + row * g.ld_y;
-  const uint64_t base = u0 * K;
+  const uint64_t t_begin = total_tiles * blockIdx.x / gridDim.x;
+  const uint64_t t_end = total_tiles * (blockIdx.x + 1) / gridDim.x;
+  // (row, tile-in-row) of the current tile, advanced incrementally (no 64-bit division)
+  uint64_t row = t_begin / tiles_per_row, tr = t_begin % tiles_per_row;
+  auto xrow = [&](uint64_t r) { return reinterpret_cast<const TV*>(g.x) + r * g.ld_x; };
+  if (t_begin < t_end) stage_tile<TV, NB * K, T>(io(0), xrow(row), g.n, tr * TU * K);
+  int cur = 0;
+  bool carried = false;                   // column 0 already holds this tile's first block
+  for (uint64_t tt = t_begin; tt < t_end; ++tt, cur ^= 1) {
+    const TV* x = xrow(row);
+    TV* y = reinterpret_cast<TV*>(g.y) + row * g.ld_y;
+    const uint64_t u0 = tr * TU;
+    uint64_t nrow = row, ntr = tr + 1;
+    if (ntr == tiles_per_row) { ntr = 0; ++nrow; }
+    cp_async_wait_all();
+    __syncthreads();                      // tile tt landed; previous tile fully consumed
+    if (tt + 1 < t_end) stage_tile<TV, NB * K, T>(io(cur ^ 1), xrow(nrow), g.n, ntr * TU * K);  // prefetch
+    TV* in = io(cur) + misalign(x + u0 * K);
 
-  // ---- load blocks u0 .. u0+T (virtual +INF padding past n) ----
-  for (uint32_t e = t; e < (uint32_t)((T + 1) * K); e += T) {
-    const uint64_t gp = base + e;
-    io[e] = gp < g.n ? Tr::enc(x[gp]) : UMax<U>::v;
-  }
-  __syncthreads();
-
-  // ---- phase 1: sort column c (= block u0+c) in registers ----
-  auto sort_column = [&](uint32_t c) {
-    E v[K];
+    // ---- phase 1: sort column c (= block u0+c) in registers ----
+    auto sort_column = [&](uint32_t c) {
+      E v[K];
 #pragma unroll
-    for (int i = 0; i < K; ++i) v[i] = E::make(io[c * K + i], (uint32_t)i);
-    sort_regs<K>(v);
+      for (int i = 0; i < K; ++i) v[i] = E::make(Tr::enc(in[c * K + i]), (uint32_t)i);
+      sort_regs<K>(v);
 #pragma unroll
-    for (int p = 0; p < K; ++p) {
-      skey[p * SC + c] = v[p].key();
-      srank[v[p].idx() * SC + c] = (uint8_t)p;
-    }
-  };
-  sort_column(t + 1);
-  if (t == 0) sort_column(0);
-  __syncthreads();
-
-  // ---- phase 2: Figure-7 postprocess for unit u = (A = column t, B = column t+1) ----
-  const uint64_t u = u0 + t;
-  uint32_t imax = 0;
-  if (u < g.units) {
-    const uint64_t rem = g.keep - u * K;
-    imax = rem < (uint64_t)K ? (uint32_t)rem : (uint32_t)K;
-  }
-  // outputs are staged in io (natural layout, odd K: conflict-free)
-  __syncthreads();  // everyone is done reading io for sorting
-  if (imax > 0) {
-    const uint32_t ca = t, cb = t + 1;
-    uint32_t maskA = (K == 32) ? 0xFFFFFFFFu : ((1u << K) - 1u);
-    uint32_t mA = H, sA = H;          // construct: s = h, m = pi[h] (block.hpp:47-49)
-    uint32_t maskB = 0, mB = K, sB = 0;  // unwind: empty, m = k, s = 0 (block.hpp:62-63)
-    U keyA = skey[mA * SC + ca];
-    U keyB = 0;
-    io[t * K] = keyA;  // Peek of the constructed block (filter.hpp:81-82)
-    for (uint32_t i = 1; i < imax; ++i) {
-      const uint32_t s = i - 1;
-      const uint32_t ra = srank[s * SC + ca];
-      const uint32_t rb = srank[s * SC + cb];
-      // Delete(A, s): block.hpp:71-87
-      maskA &= ~(1u << ra);
-      if (ra < mA) {
-        --sA;
-      } else {
-        if (ra == mA) mA = live_next(maskA, ra, K);
-        if (sA > 0) { mA = live_prev(maskA, mA, K); --sA; }
+      for (int p = 0; p < K; ++p) {
+        skey[p * SC + c] = v[p].key();
+        srank[v[p].idx() * SC + c] = (uint8_t)p;
       }
-      // Undelete(B, s): block.hpp:89-98
-      maskB |= 1u << rb;
-      if (rb < mB) mB = live_prev(maskB, mB, K);
-      // Balance: filter.hpp:90-95 (ties go to A)
-      keyA = mA < K ? skey[mA * SC + ca] : UMax<U>::v;
-      keyB = mB < K ? skey[mB * SC + cb] : UMax<U>::v;
-      if ((int)(sA + sB) < H) {
-        const bool b_less = (mB != K) && (mA == K || keyB < keyA);
-        if (!b_less) {
-          mA = (mA == K) ? live_first(maskA, K) : live_next(maskA, mA, K);
-          ++sA;
-          keyA = mA < K ? skey[mA * SC + ca] : UMax<U>::v;
-        } else {
-          mB = (mB == K) ? live_first(maskB, K) : live_next(maskB, mB, K);
-          ++sB;
-          keyB = mB < K ? skey[mB * SC + cb] : UMax<U>::v;
-        }
-      }
-      // Emit min{Peek(A), Peek(B)}: filter.hpp:97-100
-      const bool b_less = (mB != K) && (mA == K || keyB < keyA);
-      io[t * K + i] = b_less ? keyB : keyA;
-    }
-  }
-  __syncthreads();
+    };
+#pragma unroll
+    for (int j = 0; j < UPT; ++j) sort_column(t + T * j + 1);
+    if (!carried && t == 0) sort_column(0);
+    __syncthreads();                      // columns ready; `in` is free for output staging
 
-  // ---- coalesced store of the tile's contiguous outputs ----
-  const uint64_t tile_out = (uint64_t)T * K;
-  for (uint32_t e = t; e < tile_out; e += T) {
-    const uint64_t o = base + e;
-    if (o < g.keep) y[o] = Tr::dec(io[e]);
+    // ---- phase 2: Figure-7 postprocess for unit (A = column c, B = column c+1) ----
+    // Steps past the last kept output run on padding harmlessly; only the store is bounded.
+    U* ost = reinterpret_cast<U*>(in);    // natural layout, odd K: conflict-free
+#pragma unroll 1
+    for (int j = 0; j < UPT; ++j) {
+      const uint32_t c = t + T * j;
+      const U* kA = skey + c;
+      const U* kB = skey + c + 1;
+      const uint8_t* rA = srank + c;
+      const uint8_t* rB = srank + c + 1;
+      constexpr uint32_t KK = K;
+      constexpr uint32_t SENT = 1u << K;
+      uint32_t maskA = SENT | (SENT - 1u);  // construct: all live, s = h, m = pi[h] (block.hpp:47-49)
+      uint32_t mA = H, sA = H;
+      uint32_t maskB = SENT, mB = K, sB = 0;  // unwind: empty, m = k, s = 0 (block.hpp:62-63)
+      U keyA = kA[H * SC], keyB = UMax<U>::v;
+      ost[c * K] = keyA;                      // Peek of the constructed block (filter.hpp:81-82)
+#pragma unroll
+      for (int i = 1; i < K; ++i) {
+        const uint32_t ra = rA[(i - 1) * SC];
+        const uint32_t rb = rB[(i - 1) * SC];
+        // Delete(A, i-1): block.hpp:71-87
+        maskA &= ~(1u << ra);
+        const bool belowA = ra < mA;
+        const uint32_t m1 = sel(ra == mA, live_next(maskA, ra), mA);
+        const uint32_t pv = live_prev(maskA, m1, KK);
+        mA = sel(!belowA && sA > 0, pv, m1);
+        sA -= (belowA || sA > 0) ? 1u : 0u;
+        // Undelete(B, i-1): block.hpp:89-98
+        maskB |= 1u << rb;
+        mB = sel(rb < mB, live_prev(maskB, mB, KK), mB);
+        // Balance: filter.hpp:90-95 (ties go to A; the sentinel is never smaller)
+        keyA = sel(mA == KK, UMax<U>::v, kA[min(mA, KK - 1) * SC]);
+        keyB = sel(mB == KK, UMax<U>::v, kB[min(mB, KK - 1) * SC]);
+        const bool need = (int)(sA + sB) < H;
+        const bool bLess = (mB != KK) && (mA == KK || keyB < keyA);
+        const bool advA = need && !bLess, advB = need && bLess;
+        mA = sel(advA, live_succ(maskA, mA, KK), mA);
+        mB = sel(advB, live_succ(maskB, mB, KK), mB);
+        sA += advA;
+        sB += advB;
+        const U* kp = advA ? kA + min(mA, KK - 1) * SC : kB + min(mB, KK - 1) * SC;
+        const U kn = *kp;
+        keyA = sel(mA == KK, UMax<U>::v, sel(advA, kn, keyA));
+        keyB = sel(mB == KK, UMax<U>::v, sel(advB, kn, keyB));
+        // Emit min{Peek(A), Peek(B)}: filter.hpp:97-100
+        const bool bLess2 = (mB != KK) && (mA == KK || keyB < keyA);
+        ost[c * K + i] = sel(bLess2, keyB, keyA);
+      }
+    }
+    __syncthreads();
+
+    // ---- carry the tile's last block to column 0 when the next tile continues the row ----
+    carried = (nrow == row);
+    if (carried && t < (uint32_t)K) {
+      skey[t * SC] = skey[t * SC + TU];
+      srank[t * SC] = srank[t * SC + TU];
+    }
+
+    // ---- coalesced store of the tile's contiguous outputs ----
+    const uint64_t base = u0 * K;
+    const uint64_t left = g.keep > base ? g.keep - base : 0;
+    const uint32_t n_out = (uint32_t)(left < (uint64_t)TU * K ? left : (uint64_t)TU * K);
+    for (uint32_t e = t; e < n_out; e += T) y[base + e] = Tr::dec(ost[e]);
+    row = nrow;
+    tr = ntr;
   }
 }
 
