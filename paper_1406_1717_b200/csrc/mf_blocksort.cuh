@@ -1,0 +1,88 @@
+// mf_blocksort.cuh -- segmented block sort primitives (phase 1, piecewise_sort,
+// filter.hpp:41-54) shared by the medium-k and large-k pipelines.
+//
+// Elements are (key, index) pairs in one total order (mf_sortnet.cuh), so every sort
+// here is stable in the reference's sense.  A group of NT threads sorts NT*R elements:
+// each thread sorts R in registers (odd-even merge network), then log2(NT) merge-path
+// levels run through shared memory.  Shared arrays use the padded index
+// p + (p >> PS), which makes the blocked per-thread writes bank-conflict free for
+// 8-byte elements (PS = 5 when R >= 32, else 4).
+#pragma once
+#include "mf_common.cuh"
+#include "mf_sortnet.cuh"
+
+namespace mf {
+
+template <int PS>
+__device__ __forceinline__ int pad(int p) { return p + (p >> PS); }
+
+template <int R>
+constexpr int pad_shift() { return R >= 32 ? 5 : 4; }
+
+// Merge-path levels: runs of length run0, 2*run0, ... < run_end (a power-of-two
+// multiple of R) inside s[b0 .. b0 + NT*R), NT threads, thread `tid` produces the R
+// outputs [tid*R, tid*R + R) of its merged pair.  On entry s holds sorted runs of
+// length run0; v is scratch.  CTA = true syncs the CTA, else the warp.
+template <typename E, int R, int PS, bool CTA>
+__device__ __forceinline__ void merge_levels(E* s, int b0, int tid, int run0, int run_end, E (&v)[R]) {
+#pragma unroll 1
+  for (int run = run0; run < run_end; run *= 2) {
+    const int gl = (2 * run) / R;                // threads per merged run
+    const int j = tid & (gl - 1);
+    const int xb = b0 + (tid / gl) * (2 * run);  // X = [xb, xb+run), Y = [xb+run, xb+2run)
+    const int yb0 = xb + run;
+    const int d = j * R;
+    int lo = d > run ? d - run : 0, hi = d < run ? d : run;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (E::less(s[pad<PS>(xb + mid)], s[pad<PS>(yb0 + d - 1 - mid)])) lo = mid + 1; else hi = mid;
+    }
+    int ia = lo, ib = d - lo;
+    E xa = s[pad<PS>(xb + min(ia, run - 1))], yv = s[pad<PS>(yb0 + min(ib, run - 1))];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const bool takeA = (ib >= run) || (ia < run && E::less(xa, yv));
+      v[r] = takeA ? xa : yv;
+      if (takeA) { ++ia; xa = s[pad<PS>(xb + min(ia, run - 1))]; }
+      else { ++ib; yv = s[pad<PS>(yb0 + min(ib, run - 1))]; }
+    }
+    if (CTA) __syncthreads(); else __syncwarp();
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[pad<PS>(xb + d + r)] = v[r];
+    if (CTA) __syncthreads(); else __syncwarp();
+  }
+}
+
+// Warp sort of 32*R register-loaded elements (v, any distribution over lanes) into
+// s[b0 .. b0 + 32R) (padded layout, sorted ascending).
+template <typename E, int R, int PS>
+__device__ __forceinline__ void warp_sort_regs(E (&v)[R], E* s, int b0, uint32_t lane) {
+  sort_regs<R>(v);
+#pragma unroll
+  for (int r = 0; r < R; ++r) s[pad<PS>(b0 + lane * R + r)] = v[r];
+  __syncwarp();
+  merge_levels<E, R, PS, false>(s, b0, lane, R, 32 * R, v);
+}
+
+// Load block `blk` of a row (k samples from x, +INF past n, filter.hpp:28-36) with
+// coalesced loads and warp-sort it into slot sb.  Slots beyond k hold (UMAX, e >= k),
+// which sort after everything.
+template <int DT, int R>
+__device__ __forceinline__ void warp_sort_block(Elem<typename Traits<DT>::U>* sb, const typename Traits<DT>::T* x,
+                                                uint64_t n, uint32_t k, uint64_t blk, uint32_t lane) {
+  using Tr = Traits<DT>;
+  using U = typename Tr::U;
+  using E = Elem<U>;
+  E v[R];
+  const uint64_t b0 = blk * k;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t e = lane + 32 * r;
+    const uint64_t gp = b0 + e;
+    const U key = (e < k && gp < n) ? Tr::enc(__ldg(x + gp)) : UMax<U>::v;
+    v[r] = E::make(key, e);
+  }
+  warp_sort_regs<E, R, pad_shift<R>()>(v, sb, 0, lane);
+}
+
+}  // namespace mf

@@ -11,23 +11,50 @@ namespace {
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+template <int DT>
 LargeGeom plan(const Geom& g, uint64_t nb) {
+  using U = typename Traits<DT>::U;
   LargeGeom L{};
   L.g = g;
   L.nb = nb;
-  L.tiles = (g.k + LTS - 1) / LTS;
+  L.TS = TileSort<U>::TS;
+  L.tiles = (g.k + L.TS - 1) / L.TS;
+  L.mtiles = (g.k + LQ - 1) / LQ;
   L.nq = 2 * g.k;
   L.nqp = (uint32_t)align_up(L.nq, 32);
-  L.tiles2 = (L.nq + LTS - 1) / LTS;
+  L.tiles2 = (L.nq + LQ - 1) / LQ;
   // Chunk length: enough chunks per unit to fill the GPU, few enough that the
   // per-chunk selection table stays small (C * NS counters per unit).
   uint32_t cl = 64;
   while (cl < 1024 && (g.k + cl - 1) / cl > 256) cl *= 2;
-  while ((g.k + cl - 1) / cl > 4096) cl *= 2;  // bounds the per-CTA histogram (2C words)
+  while ((g.k + cl - 1) / cl > 4096) cl *= 2;  // bounds the per-CTA histogram (8C words)
   L.CL = cl;
   L.C = (g.k + cl - 1) / cl;
   L.NS = (L.nq + 1023) / 1024;
   return L;
+}
+
+// per-process kernel attributes (idempotent)
+template <int DT>
+cudaError_t configure(const LargeGeom& L) {
+  using U = typename Traits<DT>::U;
+  static bool done = false;
+  static size_t unit_merge_set = 0;
+  cudaError_t e = cudaSuccess;
+  if (!done) {
+    e = cudaFuncSetAttribute(ml_tile_sort<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TileSort<U>::smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(ml_merge_pass<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)merge_tile_smem<U>());
+    if (e != cudaSuccess) return e;
+    done = true;
+  }
+  const size_t um = merge_tile_smem<U>() + sizeof(uint32_t) * 8 * L.C;
+  if (um > unit_merge_set) {
+    e = cudaFuncSetAttribute(ml_unit_merge<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)um);
+    if (e == cudaSuccess) unit_merge_set = um;
+  }
+  return e;
 }
 
 template <int DT>
@@ -56,14 +83,17 @@ struct Layout {
 template <int DT>
 cudaError_t sort_blocks(const LargeGeom& L, unsigned char* ws, const Layout<DT>& lay, cudaStream_t s,
                         uint64_t* launches, Elem<typename Traits<DT>::U>** result) {
-  using E = Elem<typename Traits<DT>::U>;
+  using U = typename Traits<DT>::U;
+  using E = Elem<U>;
+  cudaError_t e = configure<DT>(L);
+  if (e != cudaSuccess) return e;
   E* bufs[2] = {reinterpret_cast<E*>(ws + lay.off_s0), reinterpret_cast<E*>(ws + lay.off_s1)};
-  dim3 grid((unsigned)(L.nb * L.tiles), L.g.rows);
-  ml_tile_sort<DT><<<grid, LT, 0, s>>>(L, bufs[0]);
+  ml_tile_sort<DT><<<dim3((unsigned)(L.nb * L.tiles), L.g.rows), LNT, TileSort<U>::smem, s>>>(L, bufs[0]);
   ++*launches;
   int cur = 0;
-  for (uint64_t run = LTS; run < L.g.k; run *= 2) {
-    ml_merge_pass<DT><<<grid, LT, 0, s>>>(L, bufs[cur], bufs[cur ^ 1], (uint32_t)run);
+  for (uint64_t run = L.TS; run < L.g.k; run *= 2) {
+    ml_merge_pass<DT><<<dim3((unsigned)(L.nb * L.mtiles), L.g.rows), LNT, merge_tile_smem<U>(), s>>>(
+        L, bufs[cur], bufs[cur ^ 1], (uint32_t)run);
     ++*launches;
     cur ^= 1;
   }
@@ -73,7 +103,7 @@ cudaError_t sort_blocks(const LargeGeom& L, unsigned char* ws, const Layout<DT>&
 
 template <int DT>
 cudaError_t run_large_dt(const Geom& g, void* wsv, size_t ws_bytes, cudaStream_t s, uint64_t* launches) {
-  const LargeGeom L = plan(g, g.units + 1);
+  const LargeGeom L = plan<DT>(g, g.units + 1);
   const Layout<DT> lay(L, false);
   if (ws_bytes < lay.total) return cudaErrorMemoryAllocation;
   unsigned char* ws = static_cast<unsigned char*>(wsv);
@@ -86,15 +116,13 @@ cudaError_t run_large_dt(const Geom& g, void* wsv, size_t ws_bytes, cudaStream_t
   uint2* rab = reinterpret_cast<uint2*>(ws + lay.off_rab);
   uint32_t* live = reinterpret_cast<uint32_t*>(ws + lay.off_live);
   const uint64_t nu = (uint64_t)g.rows * g.units;
-  ml_unit_merge<DT><<<dim3((unsigned)(g.units * L.tiles2), g.rows), LT, 0, s>>>(L, sorted, mk, org, rab);
-  ++*launches;
-  const size_t hist = sizeof(uint32_t) * 2 * L.C;
-  ml_counts<<<(unsigned)(nu * L.NS), LT, hist, s>>>(L, org, live);
+  const size_t um = merge_tile_smem<U>() + sizeof(uint32_t) * 8 * L.C;
+  ml_unit_merge<DT><<<dim3((unsigned)(g.units * L.tiles2), g.rows), LNT, um, s>>>(L, sorted, mk, org, rab, live);
   ++*launches;
   const uint64_t nchunks = nu * L.C;
-  ml_scan<<<(unsigned)((nchunks + LT - 1) / LT), LT, 0, s>>>(L, live, nchunks);
+  ml_scan<<<(unsigned)((nchunks + LNT - 1) / LNT), LNT, 0, s>>>(L, live, nchunks);
   ++*launches;
-  ml_walk<DT><<<(unsigned)((nchunks + LT - 1) / LT), LT, 0, s>>>(L, mk, org, rab, live, nchunks);
+  ml_walk<DT><<<(unsigned)((nchunks + LNT - 1) / LNT), LNT, 0, s>>>(L, mk, org, rab, live, nchunks);
   ++*launches;
   return cudaGetLastError();
 }
@@ -108,7 +136,7 @@ __global__ void ml_extract_perm(LargeGeom L, const Elem<typename Traits<DT>::U>*
 template <int DT>
 cudaError_t run_sort_dt(const Geom& g, uint64_t nb, void* wsv, uint32_t* perm, cudaStream_t s,
                         uint64_t* launches) {
-  const LargeGeom L = plan(g, nb);
+  const LargeGeom L = plan<DT>(g, nb);
   const Layout<DT> lay(L, true);
   using U = typename Traits<DT>::U;
   Elem<U>* sorted = nullptr;
@@ -140,12 +168,11 @@ __global__ void gen_kernel(int kind, uint64_t seed, uint64_t mod, uint64_t offse
 }  // namespace
 
 size_t large_workspace_bytes(int dt, const Geom& g) {
-  const LargeGeom L = plan(g, g.units + 1);
   switch (dt) {
-    case DT_I32: return Layout<DT_I32>(L, false).total;
-    case DT_I64: return Layout<DT_I64>(L, false).total;
-    case DT_F32: return Layout<DT_F32>(L, false).total;
-    default: return Layout<DT_F64>(L, false).total;
+    case DT_I32: return Layout<DT_I32>(plan<DT_I32>(g, g.units + 1), false).total;
+    case DT_I64: return Layout<DT_I64>(plan<DT_I64>(g, g.units + 1), false).total;
+    case DT_F32: return Layout<DT_F32>(plan<DT_F32>(g, g.units + 1), false).total;
+    default: return Layout<DT_F64>(plan<DT_F64>(g, g.units + 1), false).total;
   }
 }
 
@@ -160,12 +187,11 @@ cudaError_t run_large(int dt, const Geom& g, void* ws, size_t ws_bytes, cudaStre
 }
 
 size_t block_sort_workspace_bytes(int dt, const Geom& g, uint64_t nb) {
-  const LargeGeom L = plan(g, nb);
   switch (dt) {
-    case DT_I32: return Layout<DT_I32>(L, true).total;
-    case DT_I64: return Layout<DT_I64>(L, true).total;
-    case DT_F32: return Layout<DT_F32>(L, true).total;
-    default: return Layout<DT_F64>(L, true).total;
+    case DT_I32: return Layout<DT_I32>(plan<DT_I32>(g, nb), true).total;
+    case DT_I64: return Layout<DT_I64>(plan<DT_I64>(g, nb), true).total;
+    case DT_F32: return Layout<DT_F32>(plan<DT_F32>(g, nb), true).total;
+    default: return Layout<DT_F64>(plan<DT_F64>(g, nb), true).total;
   }
 }
 

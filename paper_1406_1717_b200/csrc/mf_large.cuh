@@ -3,15 +3,16 @@
 // the per-pair state in L2/HBM.
 //
 // Reference path replaced: median_filter<T> (filter.hpp:149-155).
-//   piecewise_sort (filter.hpp:41-54) -> segmented global merge sort: CTA tile sorts
-//       (register network + CTA merge-path passes in smem), then log2(k/TS) global
-//       merge-path passes; blocks are segments, (key, index) elements keep it stable.
+//   piecewise_sort (filter.hpp:41-54) -> segmented global merge sort: a CTA sorts a
+//       tile of TS elements (8 warp sorts + 3 CTA merge-path levels in padded smem),
+//       then ceil(log2(k/TS)) global merge-path passes; blocks are segments and the
+//       (key, index) elements keep it stable.
 //   run_postprocess (filter.hpp:64-106) -> per block pair (unit):
-//     ml_unit_merge   merge path of sorted A and sorted B (A wins key ties,
-//                     filter.hpp:92-93): merged keys, merged-position -> (block, index)
-//                     and index -> merged position (Delete(A,i) / Undelete(B,i) targets);
-//     ml_counts/ml_scan  live counts per 1024-position "superword" at every chunk start,
-//                     the selection index for the chunk's first median;
+//     ml_unit_merge   merge path of sorted A and sorted B: merged keys,
+//                     merged-position -> (block, index), index -> merged position
+//                     (the Delete(A,i) / Undelete(B,i) targets), and, fused, the live
+//                     counts of every 1024-position "superword" at every chunk start;
+//     ml_scan         prefix of those counts: the selection index for a chunk's first median;
 //     ml_walk         one thread per chunk of CL steps.  The state before step i is the
 //                     live set {A: idx >= i} u {B: idx < i} (Eq. 4 / Lemma 1,
 //                     SURVEY.md §0.6); the thread keeps only the cursor p and the one
@@ -19,153 +20,189 @@
 //                     from the origin table when the cursor leaves it, so per-thread state
 //                     is O(1) however large k is.
 #pragma once
+#include "mf_blocksort.cuh"
 #include "mf_common.cuh"
 #include "mf_sortnet.cuh"
 
 namespace mf {
 
-constexpr int LT = 256;          // threads per CTA
-constexpr int LRT = 8;           // elements per thread
-constexpr int LTS = LT * LRT;    // tile size (elements)
+constexpr int LNT = 256;         // threads per CTA
+constexpr int LR2 = 16;          // outputs per thread in merge tiles
+constexpr int LQ = LNT * LR2;    // merge tile (elements), a multiple of 1024
+constexpr int LPS = 4;           // pad shift of merge tiles (R = 16)
+template <typename U>
+constexpr size_t merge_tile_smem() { return sizeof(Elem<U>) * (LQ + (LQ >> LPS) + 1); }
+
+// tile sort geometry by key width: 8 warps x 32R elements
+template <typename U> struct TileSortCfg;
+template <> struct TileSortCfg<uint32_t> { static constexpr int R = 32; };
+template <> struct TileSortCfg<uint64_t> { static constexpr int R = 16; };
+template <typename U> struct TileSort {
+  static constexpr int R = TileSortCfg<U>::R;
+  static constexpr int PS = pad_shift<R>();
+  static constexpr int TS = 8 * 32 * R;
+  static constexpr size_t smem = sizeof(Elem<U>) * (TS + (TS >> PS) + 1);
+};
 
 struct LargeGeom {
   Geom g;
   uint64_t nb;        // blocks per row (= units + 1)
-  uint32_t tiles;     // tiles per block = ceil(k / LTS)
+  uint32_t TS;        // tile-sort size (elements)
+  uint32_t tiles;     // tile sorts per block = ceil(k / TS)
+  uint32_t mtiles;    // merge tiles per block = ceil(k / LQ)
   uint32_t nq;        // merged positions per unit = 2k
   uint32_t nqp;       // padded stride (multiple of 32)
-  uint32_t tiles2;    // tiles per unit merge = ceil(2k / LTS)
+  uint32_t tiles2;    // unit-merge tiles per unit = ceil(2k / LQ)
   uint32_t CL;        // steps per walk chunk
   uint32_t C;         // chunks per unit
   uint32_t NS;        // superwords (1024 positions) per unit
 };
 
-// CTA-wide merge passes over LTS elements in smem, runs from LRT up to LTS.
-template <typename E>
-__device__ __forceinline__ void cta_merge_passes(E* s, E (&v)[LRT]) {
-  const int tid = threadIdx.x;
-#pragma unroll 1
-  for (int run = LRT; run < LTS; run *= 2) {
-    const int gl = (2 * run) / LRT;
-    const int j = tid & (gl - 1);
-    E* X = s + (tid / gl) * (2 * run);
-    const E* Y = X + run;
-    const int d = j * LRT;
-    int lo = d > run ? d - run : 0, hi = d < run ? d : run;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (E::less(X[mid], Y[d - 1 - mid])) lo = mid + 1; else hi = mid;
-    }
-    int ia = lo, ib = d - lo;
-    E xa = X[ia < run ? ia : run - 1], yb = Y[ib < run ? ib : run - 1];
-#pragma unroll
-    for (int r = 0; r < LRT; ++r) {
-      const bool takeA = (ib >= run) || (ia < run && E::less(xa, yb));
-      v[r] = takeA ? xa : yb;
-      if (takeA) { ++ia; xa = X[ia < run ? ia : run - 1]; }
-      else { ++ib; yb = Y[ib < run ? ib : run - 1]; }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < LRT; ++r) X[d + r] = v[r];
-    __syncthreads();
-  }
-}
-
-// ---- phase 1a: sort LTS-element tiles of every block ---------------------------------
+// ---- phase 1a: sort TS-element tiles of every block ----------------------------------
 template <int DT>
-__global__ void __launch_bounds__(LT) ml_tile_sort(LargeGeom L, Elem<typename Traits<DT>::U>* out) {
+__global__ void __launch_bounds__(LNT) ml_tile_sort(LargeGeom L, Elem<typename Traits<DT>::U>* out) {
   using Tr = Traits<DT>;
   using U = typename Tr::U;
   using E = Elem<U>;
   using TV = typename Tr::T;
-  __shared__ E s[LTS];
+  using C = TileSort<U>;
+  constexpr int R = C::R, PS = C::PS, TS = C::TS;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  E* s = reinterpret_cast<E*>(smem_raw);
   const Geom& g = L.g;
   const uint64_t row = blockIdx.y;
   const uint64_t b = blockIdx.x / L.tiles;
   const uint32_t t = blockIdx.x % L.tiles;
   const TV* x = reinterpret_cast<const TV*>(g.x) + row * g.ld_x;
   const uint32_t k = g.k;
-  E v[LRT];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  E v[R];
 #pragma unroll
-  for (int r = 0; r < LRT; ++r) {
-    const uint32_t e = t * LTS + threadIdx.x + LT * r;
+  for (int r = 0; r < R; ++r) {
+    const uint32_t e = t * TS + warp * 32 * R + lane + 32 * r;  // coalesced across the warp
     const uint64_t gp = b * k + e;
-    const U key = (e < k && gp < g.n) ? Tr::enc(x[gp]) : UMax<U>::v;
+    const U key = (e < k && gp < g.n) ? Tr::enc(__ldg(x + gp)) : UMax<U>::v;
     v[r] = E::make(key, e);
   }
-  sort_regs<LRT>(v);
-#pragma unroll
-  for (int r = 0; r < LRT; ++r) s[threadIdx.x * LRT + r] = v[r];
+  warp_sort_regs<E, R, PS>(v, s, warp * 32 * R, lane);
   __syncthreads();
-  cta_merge_passes<E>(s, v);
-  const uint32_t len = min((uint32_t)LTS, k - t * LTS);
-  E* o = out + (row * L.nb + b) * k + (uint64_t)t * LTS;
-  for (uint32_t i = threadIdx.x; i < len; i += LT) o[i] = s[i];
+  merge_levels<E, R, PS, true>(s, 0, threadIdx.x, 32 * R, TS, v);
+  const uint32_t len = min((uint32_t)TS, k - t * TS);
+  E* o = out + (row * L.nb + b) * k + (uint64_t)t * TS;
+  for (uint32_t i = threadIdx.x; i < len; i += LNT) o[i] = s[pad<PS>(i)];
 }
 
-// merge-path split of diagonal d over X[0,lx) and Y[0,ly) under `before(x, y)`
+// Warp-cooperative merge-path split: the number of X elements among the first d merged
+// elements of X[0,lx) and Y[0,ly) under `before(x, y)` (x goes first).  Each round probes
+// 32 diagonal points at once, so a split over 10^5 costs 4 rounds of loads, not 17.
 template <typename E, typename Before>
-__device__ __forceinline__ uint32_t merge_split(const E* X, uint32_t lx, const E* Y, uint32_t ly,
-                                                uint32_t d, Before before) {
+__device__ __forceinline__ uint32_t warp_split(const E* X, uint32_t lx, const E* Y, uint32_t ly, uint32_t d,
+                                               Before before, uint32_t lane) {
   uint32_t lo = d > ly ? d - ly : 0, hi = d < lx ? d : lx;
   while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (before(X[mid], Y[d - 1 - mid])) lo = mid + 1; else hi = mid;
+    const uint32_t step = (hi - lo + 31) / 32;
+    const uint32_t mid = lo + lane * step;
+    const bool p = mid < hi && before(X[mid], Y[d - 1 - mid]);
+    const uint32_t c = __popc(__ballot_sync(0xFFFFFFFFu, p));  // a prefix of lanes: monotone
+    const uint32_t nlo = c ? lo + (c - 1) * step + 1 : lo;
+    hi = min(hi, lo + c * step);
+    lo = nlo;
   }
   return lo;
 }
 
-// ---- phase 1b: one global merge pass (runs of length `run` within every block) --------
-template <int DT>
-__global__ void __launch_bounds__(LT) ml_merge_pass(LargeGeom L, const Elem<typename Traits<DT>::U>* in,
-                                                    Elem<typename Traits<DT>::U>* out, uint32_t run) {
-  using U = typename Traits<DT>::U;
-  using E = Elem<U>;
-  __shared__ E sx[LTS];
-  __shared__ uint32_t split[2];
-  const uint64_t row = blockIdx.y;
-  const uint64_t b = blockIdx.x / L.tiles;
-  const uint32_t t = blockIdx.x % L.tiles;
-  const uint32_t k = L.g.k;
-  const uint64_t base = (row * L.nb + b) * k;
-  const uint32_t p0 = t * LTS;
-  const uint32_t x0 = p0 / (2 * run) * (2 * run);
-  const uint32_t lx = min(run, k - x0);
-  const uint32_t y0 = x0 + lx;
-  const uint32_t ly = y0 < k ? min(run, k - y0) : 0;
-  const E* X = in + base + x0;
-  const E* Y = in + base + y0;
-  const uint32_t d0 = p0 - x0;
-  const uint32_t d1 = min(d0 + LTS, lx + ly);
-  auto before = [](const E& a, const E& c) { return E::less(a, c); };
-  if (threadIdx.x < 2) split[threadIdx.x] = merge_split(X, lx, Y, ly, threadIdx.x ? d1 : d0, before);
+// One LQ-output tile of a merge of X[0,lx) and Y[0,ly), outputs [d0, d1): the inputs go
+// through padded smem; thread `tid` merges outputs [tid*LR2, tid*LR2 + LR2) into v and
+// returns how many it produced; `srcB[r]` tells which side each came from.
+template <typename E, typename Before>
+__device__ __forceinline__ int merge_tile(E* s, const E* X, uint32_t lx, const E* Y, uint32_t ly, uint32_t d0,
+                                          uint32_t d1, Before before, E (&v)[LR2], bool (&srcB)[LR2],
+                                          uint32_t* split, uint32_t& nx_out) {
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < 2) {
+    const uint32_t a = warp_split(X, lx, Y, ly, warp ? d1 : d0, before, lane);
+    if (lane == 0) split[warp] = a;
+  }
   __syncthreads();
   const uint32_t a0 = split[0], a1 = split[1];
   const uint32_t b0 = d0 - a0, b1 = d1 - a1;
   const uint32_t nx = a1 - a0, ny = b1 - b0;
-  for (uint32_t i = threadIdx.x; i < nx + ny; i += LT) sx[i] = i < nx ? X[a0 + i] : Y[b0 + i - nx];
+  for (uint32_t i = threadIdx.x; i < nx + ny; i += LNT) s[pad<LPS>(i)] = i < nx ? X[a0 + i] : Y[b0 + i - nx];
   __syncthreads();
-  const E* SX = sx;
-  const E* SY = sx + nx;
-  const uint32_t dd = threadIdx.x * LRT;
-  if (dd < nx + ny) {
-    uint32_t ia = merge_split(SX, nx, SY, ny, dd, before), ib = dd - ia;
-    E* o = out + base + x0 + d0 + dd;
-    for (int r = 0; r < LRT && dd + r < nx + ny; ++r) {
-      const bool takeA = (ib >= ny) || (ia < nx && E::less(SX[ia], SY[ib]));
-      o[r] = takeA ? SX[ia++] : SY[ib++];
+  nx_out = nx;
+  const int dd = threadIdx.x * LR2;
+  const int tot = (int)(nx + ny);
+  int cnt = 0;
+  if (dd < tot) {
+    const int NX = (int)nx, NY = (int)ny;
+    int lo = dd > NY ? dd - NY : 0, hi = dd < NX ? dd : NX;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (before(s[pad<LPS>(mid)], s[pad<LPS>(NX + dd - 1 - mid)])) lo = mid + 1; else hi = mid;
+    }
+    int ia = lo, ib = dd - lo;
+    E xa = s[pad<LPS>(min(ia, max(NX - 1, 0)))], yv = s[pad<LPS>(NX + min(ib, max(NY - 1, 0)))];
+    cnt = min(LR2, tot - dd);
+#pragma unroll
+    for (int r = 0; r < LR2; ++r) {
+      if (r < cnt) {
+        const bool takeA = (ib >= NY) || (ia < NX && before(xa, yv));
+        v[r] = takeA ? xa : yv;
+        srcB[r] = !takeA;
+        if (takeA) { ++ia; xa = s[pad<LPS>(min(ia, max(NX - 1, 0)))]; }
+        else { ++ib; yv = s[pad<LPS>(NX + min(ib, max(NY - 1, 0)))]; }
+      }
     }
   }
+  return cnt;
 }
 
-// ---- phase 2a: merge each pair (A = block u, B = block u+1) ---------------------------
+// ---- phase 1b: one global merge pass (runs of length `run` within every block) --------
 template <int DT>
-__global__ void __launch_bounds__(LT) ml_unit_merge(LargeGeom L, const Elem<typename Traits<DT>::U>* S,
-                                                    typename Traits<DT>::U* mk, uint32_t* org, uint2* rab) {
+__global__ void __launch_bounds__(LNT) ml_merge_pass(LargeGeom L, const Elem<typename Traits<DT>::U>* in,
+                                                     Elem<typename Traits<DT>::U>* out, uint32_t run) {
   using U = typename Traits<DT>::U;
   using E = Elem<U>;
-  __shared__ E sx[LTS];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  E* s = reinterpret_cast<E*>(smem_raw);
+  __shared__ uint32_t split[2];
+  const uint64_t row = blockIdx.y;
+  const uint64_t b = blockIdx.x / L.mtiles;
+  const uint32_t t = blockIdx.x % L.mtiles;
+  const uint32_t k = L.g.k;
+  const uint64_t base = (row * L.nb + b) * k;
+  const uint32_t p0 = t * LQ;
+  const uint32_t x0 = p0 / (2 * run) * (2 * run);
+  const uint32_t lx = min(run, k - x0);
+  const uint32_t y0 = x0 + lx;
+  const uint32_t ly = y0 < k ? min(run, k - y0) : 0;
+  const uint32_t d0 = p0 - x0;
+  const uint32_t d1 = min(d0 + LQ, lx + ly);
+  auto before = [](const E& a, const E& c) { return E::less(a, c); };
+  E v[LR2];
+  bool srcB[LR2];
+  uint32_t nx;
+  const int cnt = merge_tile(s, in + base + x0, lx, in + base + y0, ly, d0, d1, before, v, srcB, split, nx);
+  __syncthreads();
+  const int dd = threadIdx.x * LR2;
+#pragma unroll
+  for (int r = 0; r < LR2; ++r)
+    if (r < cnt) s[pad<LPS>(dd + r)] = v[r];
+  __syncthreads();
+  E* o = out + base + x0 + d0;
+  for (uint32_t i = threadIdx.x; i < d1 - d0; i += LNT) o[i] = s[pad<LPS>(i)];
+}
+
+// ---- phase 2a: merge each pair (A = block u, B = block u+1) + live counts -------------
+template <int DT>
+__global__ void __launch_bounds__(LNT) ml_unit_merge(LargeGeom L, const Elem<typename Traits<DT>::U>* S,
+                                                     typename Traits<DT>::U* mk, uint32_t* org, uint2* rab,
+                                                     uint32_t* live) {
+  using U = typename Traits<DT>::U;
+  using E = Elem<U>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  E* s = reinterpret_cast<E*>(smem_raw);                                     // merge tile
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw + sizeof(E) * (LQ + (LQ >> LPS) + 1));  // [4][2][C]
   __shared__ uint32_t split[2];
   const uint64_t row = blockIdx.y;
   const uint64_t u = blockIdx.x / L.tiles2;
@@ -174,67 +211,71 @@ __global__ void __launch_bounds__(LT) ml_unit_merge(LargeGeom L, const Elem<type
   const E* A = S + (row * L.nb + u) * k;
   const E* B = A + k;
   const uint64_t ug = row * L.g.units + u;
-  const uint32_t d0 = t * LTS, d1 = min(d0 + LTS, L.nq);
-  auto before = [](const E& a, const E& c) { return a.key() <= c.key(); };  // A wins ties
-  if (threadIdx.x < 2) split[threadIdx.x] = merge_split(A, k, B, k, threadIdx.x ? d1 : d0, before);
+  const uint32_t d0 = t * LQ, d1 = min(d0 + LQ, L.nq);
+  const uint32_t C = L.C;
+  for (uint32_t i = threadIdx.x; i < 8 * C; i += LNT) hist[i] = 0;
+  auto before = [](const E& a, const E& c) { return a.key() <= c.key(); };  // A first on key ties
+  E v[LR2];
+  bool srcB[LR2];
+  uint32_t nx;
+  const int cnt = merge_tile(s, A, k, B, k, d0, d1, before, v, srcB, split, nx);
+  const int dd = threadIdx.x * LR2;
+  uint2* ro = rab + ug * k;
   __syncthreads();
-  const uint32_t a0 = split[0], a1 = split[1];
-  const uint32_t b0 = d0 - a0, b1 = d1 - a1;
-  const uint32_t nx = a1 - a0, ny = b1 - b0;
-  for (uint32_t i = threadIdx.x; i < nx + ny; i += LT) sx[i] = i < nx ? A[a0 + i] : B[b0 + i - nx];
-  __syncthreads();
-  const E* SX = sx;
-  const E* SY = sx + nx;
-  const uint32_t dd = threadIdx.x * LRT;
-  if (dd < nx + ny) {
-    uint32_t ia = merge_split(SX, nx, SY, ny, dd, before), ib = dd - ia;
-    U* mko = mk + ug * L.nqp + d0 + dd;
-    uint32_t* oo = org + ug * L.nqp + d0 + dd;
-    uint2* ro = rab + ug * k;
-    for (int r = 0; r < LRT && dd + r < nx + ny; ++r) {
+  U* sk = reinterpret_cast<U*>(s);                          // staging: keys, then origins
+  uint32_t* so = reinterpret_cast<uint32_t*>(sk + LQ);
+#pragma unroll
+  for (int r = 0; r < LR2; ++r) {
+    if (r < cnt) {
       const uint32_t q = d0 + dd + r;
-      const bool takeA = (ib >= ny) || (ia < nx && SX[ia].key() <= SY[ib].key());
-      const E e = takeA ? SX[ia++] : SY[ib++];
-      mko[r] = e.key();
-      oo[r] = e.idx() | (takeA ? 0u : 0x80000000u);
-      if (takeA) ro[e.idx()].x = q; else ro[e.idx()].y = q;
+      const uint32_t idx = v[r].idx();
+      sk[dd + r] = v[r].key();
+      so[dd + r] = idx | (srcB[r] ? 0x80000000u : 0u);
+      if (srcB[r]) ro[idx].y = q; else ro[idx].x = q;
+      const uint32_t sw = (dd + r) >> 10;                   // superword within the tile
+      atomicAdd(&hist[(sw * 2 + (srcB[r] ? 1 : 0)) * C + idx / L.CL], 1u);
+    }
+  }
+  __syncthreads();
+  U* mko = mk + ug * L.nqp + d0;
+  uint32_t* oo = org + ug * L.nqp + d0;
+  for (uint32_t i = threadIdx.x; i < d1 - d0; i += LNT) { mko[i] = sk[i]; oo[i] = so[i]; }
+  // live count of each superword at every chunk start c: A elements with chunk >= c plus
+  // B elements with chunk < c.  One warp per superword; lanes scan 32 chunks at a time.
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t nsw = (d1 - d0 + 1023) / 1024;
+  if (warp < nsw) {
+    const uint32_t* hA = hist + (warp * 2) * C;
+    const uint32_t* hB = hist + (warp * 2 + 1) * C;
+    const uint32_t S = d0 / 1024 + warp;
+    uint32_t totA = 0;
+    for (uint32_t c = lane; c < C; c += 32) totA += hA[c];
+    for (int o = 16; o; o >>= 1) totA += __shfl_xor_sync(0xFFFFFFFFu, totA, o);
+    uint32_t preA = 0, preB = 0;  // exclusive prefixes over chunks < c0
+    for (uint32_t c0 = 0; c0 < C; c0 += 32) {
+      const uint32_t c = c0 + lane;
+      const uint32_t a = c < C ? hA[c] : 0, bb = c < C ? hB[c] : 0;
+      uint32_t ia = a, ib = bb;  // inclusive warp scans
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t ta = __shfl_up_sync(0xFFFFFFFFu, ia, o), tb = __shfl_up_sync(0xFFFFFFFFu, ib, o);
+        if (lane >= (uint32_t)o) { ia += ta; ib += tb; }
+      }
+      if (c < C) live[(ug * L.NS + S) * C + c] = (totA - (preA + ia - a)) + (preB + ib - bb);
+      preA += __shfl_sync(0xFFFFFFFFu, ia, 31);
+      preB += __shfl_sync(0xFFFFFFFFu, ib, 31);
     }
   }
 }
 
-// ---- phase 2b: live counts per (chunk start, superword) ------------------------------
-__global__ void __launch_bounds__(LT) ml_counts(LargeGeom L, const uint32_t* org, uint32_t* live) {
-  extern __shared__ uint32_t hist[];  // hA[C], hB[C]
-  const uint64_t ug = blockIdx.x / L.NS;
-  const uint32_t S = blockIdx.x % L.NS;
-  uint32_t* hA = hist;
-  uint32_t* hB = hist + L.C;
-  for (uint32_t c = threadIdx.x; c < 2 * L.C; c += LT) hist[c] = 0;
-  __syncthreads();
-  const uint32_t* og = org + ug * L.nqp;
-  const uint32_t q1 = min((S + 1) * 1024u, L.nq);
-  for (uint32_t q = S * 1024 + threadIdx.x; q < q1; q += LT) {
-    const uint32_t v = og[q];
-    const uint32_t c = (v & 0x7FFFFFFFu) / L.CL;
-    atomicAdd((v >> 31) ? &hB[c] : &hA[c], 1u);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {  // hA -> suffix sums, hB -> exclusive prefix sums
-    uint32_t acc = 0;
-    for (int c = (int)L.C - 1; c >= 0; --c) { acc += hA[c]; hA[c] = acc; }
-    acc = 0;
-    for (uint32_t c = 0; c < L.C; ++c) { const uint32_t t = hB[c]; hB[c] = acc; acc += t; }
-  }
-  __syncthreads();
-  for (uint32_t c = threadIdx.x; c < L.C; c += LT) live[(ug * L.C + c) * L.NS + S] = hA[c] + hB[c];
-}
-
+// exclusive prefix over superwords of the live counts, per (unit, chunk)
 __global__ void ml_scan(LargeGeom L, uint32_t* live, uint64_t total) {
   const uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= total) return;
-  uint32_t* p = live + id * L.NS;
+  const uint64_t ug = id / L.C;
+  const uint32_t c = id % L.C;
+  uint32_t* p = live + ug * L.NS * L.C + c;
   uint32_t acc = 0;
-  for (uint32_t S = 0; S < L.NS; ++S) { const uint32_t t = p[S]; p[S] = acc; acc += t; }
+  for (uint32_t S = 0; S < L.NS; ++S) { const uint32_t t = p[S * L.C]; p[S * L.C] = acc; acc += t; }
 }
 
 // live bits of merged positions [32w, 32w+32) just before step i (output i)
@@ -259,8 +300,8 @@ __device__ __forceinline__ uint32_t live_word(const uint32_t* og, uint32_t w, ui
 
 // ---- phase 2c: chunked walk -----------------------------------------------------------
 template <int DT>
-__global__ void __launch_bounds__(LT) ml_walk(LargeGeom L, const typename Traits<DT>::U* mk, const uint32_t* org,
-                                              const uint2* rab, const uint32_t* live, uint64_t total) {
+__global__ void __launch_bounds__(LNT) ml_walk(LargeGeom L, const typename Traits<DT>::U* mk, const uint32_t* org,
+                                               const uint2* rab, const uint32_t* live, uint64_t total) {
   using Tr = Traits<DT>;
   using U = typename Tr::U;
   using TV = typename Tr::T;
@@ -279,16 +320,16 @@ __global__ void __launch_bounds__(LT) ml_walk(LargeGeom L, const typename Traits
   const uint32_t* og = org + ug * L.nqp;
   const U* mkg = mk + ug * L.nqp;
   const uint2* rb = rab + ug * k;
-  const uint32_t* cum = live + (ug * L.C + c) * L.NS;
+  const uint32_t* cum = live + ug * L.NS * L.C + c;   // stride C over superwords
   TV* y = reinterpret_cast<TV*>(g.y) + row * g.ld_y + u * k;
 
   // select: superword with cum[S] <= h < cum[S+1], then words inside it
   uint32_t lo = 0, hi = L.NS - 1;
   while (lo < hi) {
     const uint32_t mid = (lo + hi + 1) >> 1;
-    if (__ldg(cum + mid) <= h) lo = mid; else hi = mid - 1;
+    if (__ldg(cum + mid * L.C) <= h) lo = mid; else hi = mid - 1;
   }
-  uint32_t r = h - __ldg(cum + lo);
+  uint32_t r = h - __ldg(cum + lo * L.C);
   uint32_t cw = lo * 32, cb = 0;
   for (;; ++cw) {
     cb = live_word(og, cw, i0, L.nq);
@@ -303,16 +344,14 @@ __global__ void __launch_bounds__(LT) ml_walk(LargeGeom L, const typename Traits
     const uint32_t a = ab.x, b = ab.y;
     if ((a >> 5) == cw) cb &= ~(1u << (a & 31));
     if ((b >> 5) == cw) cb |= 1u << (b & 31);
-    int dir = 0;
-    if (a == p) dir = b < p ? -1 : 1;
-    else if (a < p && b > p) dir = 1;
-    else if (a > p && b < p) dir = -1;
-    if (dir > 0) {
+    const bool up = (a == p) ? (b > p) : (a < p && b > p);
+    const bool down = (a == p) ? (b < p) : (a > p && b < p);
+    if (up) {
       const uint32_t sh = (p & 31) + 1;
       uint32_t m = sh < 32 ? cb & (0xFFFFFFFFu << sh) : 0;
       while (m == 0) { ++cw; cb = live_word(og, cw, i, L.nq); m = cb; }
       p = cw * 32 + __ffs(m) - 1;
-    } else if (dir < 0) {
+    } else if (down) {
       uint32_t m = cb & ((1u << (p & 31)) - 1u);
       while (m == 0) { --cw; cb = live_word(og, cw, i, L.nq); m = cb; }
       p = cw * 32 + 31 - __clz(m);

@@ -29,6 +29,7 @@
 // median is written once, coalesced.
 #pragma once
 #include "mf_common.cuh"
+#include "mf_blocksort.cuh"
 #include "mf_sortnet.cuh"
 
 namespace mf {
@@ -41,7 +42,7 @@ struct MediumCfg {
   static constexpr int BS = 32 * R;        // block slot capacity (>= k)
   static constexpr int NW = 2 * R;         // words per merged row (2k bits <= 64R)
   // padded element index: blocked per-lane writes hit distinct banks (8-byte elements)
-  static constexpr int PS = (R >= 32) ? 5 : 4;
+  static constexpr int PS = pad_shift<R>();
   static constexpr int SLOT = BS + (BS >> PS) + 1;
   static constexpr size_t sz_sorted = sizeof(E) * SLOT * (W + 1);
   static constexpr size_t sz_src = sizeof(uint16_t) * 2 * BS;  // merged pos -> (isB, sorted pos)
@@ -55,61 +56,9 @@ struct MediumCfg {
   static constexpr size_t smem = sz_sorted + W * sz_warp;
 };
 
-template <int PS>
-__device__ __forceinline__ int pad(int p) { return p + (p >> PS); }
-
 // rows[L][w] lives at w*32 + (L ^ (w & 31)): the prefix pass (lane = word, loop
 // over L) and the walk (lane = L, data-dependent word) are both bank-spread.
 __device__ __forceinline__ uint32_t row_addr(uint32_t L, uint32_t w) { return w * 32 + (L ^ (w & 31)); }
-
-// Warp-wide sort of block `blk` into slot `sb` (padded layout).
-template <int DT, int R, int PS>
-__device__ __forceinline__ void warp_sort_block(Elem<typename Traits<DT>::U>* sb, const typename Traits<DT>::T* x,
-                                                uint64_t n, uint32_t k, uint64_t blk, uint32_t lane) {
-  using Tr = Traits<DT>;
-  using U = typename Tr::U;
-  using E = Elem<U>;
-  constexpr int BS = 32 * R;
-  E v[R];
-  const uint64_t b0 = blk * k;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const uint32_t e = lane + 32 * r;            // coalesced across the warp
-    const uint64_t gp = b0 + e;
-    const U key = (e < k && gp < n) ? Tr::enc(__ldg(x + gp)) : UMax<U>::v;
-    v[r] = E::make(key, e);                      // padding: (UMAX, e) sorts last
-  }
-  sort_regs<R>(v);
-#pragma unroll
-  for (int r = 0; r < R; ++r) sb[pad<PS>(lane * R + r)] = v[r];
-  __syncwarp();
-#pragma unroll 1
-  for (int run = R; run < BS; run *= 2) {
-    const int gl = (2 * run) / R;                // lanes per merged run
-    const int j = lane & (gl - 1);
-    const int xb = (lane / gl) * (2 * run);      // X = [xb, xb+run), Y = [xb+run, xb+2run)
-    const int yb0 = xb + run;
-    const int d = j * R;
-    int lo = d > run ? d - run : 0, hi = d < run ? d : run;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (E::less(sb[pad<PS>(xb + mid)], sb[pad<PS>(yb0 + d - 1 - mid)])) lo = mid + 1; else hi = mid;
-    }
-    int ia = lo, ib = d - lo;
-    E xa = sb[pad<PS>(xb + min(ia, run - 1))], yv = sb[pad<PS>(yb0 + min(ib, run - 1))];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const bool takeA = (ib >= run) || (ia < run && E::less(xa, yv));
-      v[r] = takeA ? xa : yv;
-      if (takeA) { ++ia; xa = sb[pad<PS>(xb + min(ia, run - 1))]; }
-      else { ++ib; yv = sb[pad<PS>(yb0 + min(ib, run - 1))]; }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < R; ++r) sb[pad<PS>(xb + d + r)] = v[r];
-    __syncwarp();
-  }
-}
 
 template <int DT, int R, int W>
 __global__ void __launch_bounds__(32 * W) mf_medium_kernel(Geom g, uint64_t tiles_per_row, uint64_t total_tiles) {
@@ -147,8 +96,8 @@ __global__ void __launch_bounds__(32 * W) mf_medium_kernel(Geom g, uint64_t tile
     auto slot = [&](uint32_t logical) { return ring + ((base + logical) % (W + 1)) * SLOT; };
 
     // ---------------- phase 1: warp block sorts ----------------
-    if (!carry && warp == 0) warp_sort_block<DT, R, PS>(slot(0), x, g.n, k, u0, lane);
-    warp_sort_block<DT, R, PS>(slot(warp + 1), x, g.n, k, u0 + warp + 1, lane);
+    if (!carry && warp == 0) warp_sort_block<DT, R>(slot(0), x, g.n, k, u0, lane);
+    warp_sort_block<DT, R>(slot(warp + 1), x, g.n, k, u0 + warp + 1, lane);
     __syncthreads();
 
     // ---------------- phase 2: per-pair postprocess ----------------
