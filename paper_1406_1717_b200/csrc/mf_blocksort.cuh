@@ -41,10 +41,15 @@ __device__ __forceinline__ void merge_levels(E* s, int b0, int tid, int run0, in
     E xa = s[pad<PS>(xb + min(ia, run - 1))], yv = s[pad<PS>(yb0 + min(ib, run - 1))];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
+      // branch-free step: one shared load refills whichever side was consumed
       const bool takeA = (ib >= run) || (ia < run && E::less(xa, yv));
-      v[r] = takeA ? xa : yv;
-      if (takeA) { ++ia; xa = s[pad<PS>(xb + min(ia, run - 1))]; }
-      else { ++ib; yv = s[pad<PS>(yb0 + min(ib, run - 1))]; }
+      v[r] = E::select(takeA, xa, yv);
+      ia += takeA;
+      ib += !takeA;
+      const int nidx = takeA ? xb + min(ia, run - 1) : yb0 + min(ib, run - 1);
+      const E nv = s[pad<PS>(nidx)];
+      xa = E::select(takeA, nv, xa);
+      yv = E::select(takeA, yv, nv);
     }
     if (CTA) __syncthreads(); else __syncwarp();
 #pragma unroll

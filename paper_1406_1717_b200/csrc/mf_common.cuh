@@ -72,4 +72,19 @@ struct Geom {
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
+// Forced select (selp): both operands are computed, so no divergent branch is emitted.
+__device__ __forceinline__ uint32_t sel(bool c, uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\tselp.b32 %0, %2, %3, p;\n\t}"
+      : "=r"(r) : "r"((uint32_t)c), "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t sel(bool c, uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\tselp.b64 %0, %2, %3, p;\n\t}"
+      : "=l"(r) : "r"((uint32_t)c), "l"(a), "l"(b));
+  return r;
+}
+
+
 }  // namespace mf

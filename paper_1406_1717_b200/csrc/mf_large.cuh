@@ -141,17 +141,19 @@ __device__ __forceinline__ int merge_tile(E* s, const E* X, uint32_t lx, const E
       if (before(s[pad<LPS>(mid)], s[pad<LPS>(NX + dd - 1 - mid)])) lo = mid + 1; else hi = mid;
     }
     int ia = lo, ib = dd - lo;
-    E xa = s[pad<LPS>(min(ia, max(NX - 1, 0)))], yv = s[pad<LPS>(NX + min(ib, max(NY - 1, 0)))];
+    const int lastX = max(NX - 1, 0), lastY = NX + max(NY - 1, 0);
+    E xa = s[pad<LPS>(min(ia, lastX))], yv = s[pad<LPS>(min(NX + ib, lastY))];
     cnt = min(LR2, tot - dd);
 #pragma unroll
     for (int r = 0; r < LR2; ++r) {
-      if (r < cnt) {
-        const bool takeA = (ib >= NY) || (ia < NX && before(xa, yv));
-        v[r] = takeA ? xa : yv;
-        srcB[r] = !takeA;
-        if (takeA) { ++ia; xa = s[pad<LPS>(min(ia, max(NX - 1, 0)))]; }
-        else { ++ib; yv = s[pad<LPS>(NX + min(ib, max(NY - 1, 0)))]; }
-      }
+      const bool takeA = (ib >= NY) || (ia < NX && before(xa, yv));
+      v[r] = E::select(takeA, xa, yv);
+      srcB[r] = !takeA;
+      ia += takeA;
+      ib += !takeA;
+      const E nv = s[pad<LPS>(takeA ? min(ia, lastX) : min(NX + ib, lastY))];
+      xa = E::select(takeA, nv, xa);
+      yv = E::select(takeA, yv, nv);
     }
   }
   return cnt;

@@ -46,20 +46,6 @@ struct SmallCfg {
   static constexpr size_t smem = off_io + 2 * (size_t)IO;
 };
 
-// Forced select (selp): both operands are computed, so no divergent branch is emitted.
-__device__ __forceinline__ uint32_t sel(bool c, uint32_t a, uint32_t b) {
-  uint32_t r;
-  asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\tselp.b32 %0, %2, %3, p;\n\t}"
-      : "=r"(r) : "r"((uint32_t)c), "r"(a), "r"(b));
-  return r;
-}
-__device__ __forceinline__ uint64_t sel(bool c, uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\tselp.b64 %0, %2, %3, p;\n\t}"
-      : "=l"(r) : "r"((uint32_t)c), "l"(a), "l"(b));
-  return r;
-}
-
 // Live masks carry a sentinel bit at position K (the reference's list node k,
 // block.hpp:21-24), so "next live" always exists and needs no branch.
 __device__ __forceinline__ uint32_t live_next(uint32_t mask, uint32_t r) {

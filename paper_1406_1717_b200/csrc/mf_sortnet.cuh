@@ -13,6 +13,8 @@
 #pragma once
 #include <cstdint>
 
+#include "mf_common.cuh"
+
 namespace mf {
 
 struct NetList {
@@ -59,6 +61,9 @@ template <> struct Elem<uint32_t> {
     const uint64_t hi = x.v < y.v ? y.v : x.v;
     x.v = lo; y.v = hi;
   }
+  __device__ __forceinline__ static Elem select(bool c, const Elem& a, const Elem& b) {
+    Elem e; e.v = sel(c, a.v, b.v); return e;
+  }
 };
 
 template <> struct Elem<uint64_t> {
@@ -77,6 +82,9 @@ template <> struct Elem<uint64_t> {
     const Elem t = x;
     x.k = sw ? y.k : x.k; x.i = sw ? y.i : x.i;
     y.k = sw ? t.k : y.k; y.i = sw ? t.i : y.i;
+  }
+  __device__ __forceinline__ static Elem select(bool c, const Elem& a, const Elem& b) {
+    Elem e; e.k = sel(c, a.k, b.k); e.i = sel(c, a.i, b.i); return e;
   }
 };
 
