@@ -6,9 +6,10 @@ import subprocess
 import sys
 
 rep, kern = sys.argv[1], sys.argv[2]
+skip = sys.argv[4] if len(sys.argv) > 4 else "0"
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
-                      "-k", f"regex:{kern}", "-c", "1"], capture_output=True, text=True).stdout
+                      "-k", f"regex:{kern}", "--launch-skip", skip, "-c", "1"], capture_output=True, text=True).stdout
 rows, fname, header = [], None, None
 for rec in csv.reader(io.StringIO(out)):
     if not rec:
