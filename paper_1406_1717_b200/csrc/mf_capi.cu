@@ -5,6 +5,7 @@
 // fallback: every entry either runs the CUDA kernels or returns an error status.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -21,6 +22,9 @@ struct mf_context {
   size_t io_bytes = 0;
   int force_class = MF_CLASS_AUTO;
   uint64_t launches = 0;
+  // host-entry pipeline: H2D / compute / D2H on three streams, kNumSlots chunks in flight
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_in[3] = {}, ev_done[3] = {}, ev_out[3] = {};
   std::mutex mu;
 };
 
@@ -159,6 +163,13 @@ void mf_context_destroy(mf_context* ctx) {
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->io) cudaFree(ctx->io);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->s_h2d) cudaStreamSynchronize(ctx->s_h2d), cudaStreamDestroy(ctx->s_h2d);
+  if (ctx->s_d2h) cudaStreamSynchronize(ctx->s_d2h), cudaStreamDestroy(ctx->s_d2h);
+  for (int i = 0; i < 3; ++i) {
+    if (ctx->ev_in[i]) cudaEventDestroy(ctx->ev_in[i]);
+    if (ctx->ev_done[i]) cudaEventDestroy(ctx->ev_done[i]);
+    if (ctx->ev_out[i]) cudaEventDestroy(ctx->ev_out[i]);
+  }
   delete ctx;
 }
 
@@ -190,6 +201,11 @@ mf_status mf_median_filter_device(mf_context* ctx, mf_dtype dtype, const void* d
   return mf_median_filter_rows_device(ctx, dtype, d_x, 1, n, n, k, d_y, keep ? keep : 1, stream);
 }
 
+// Host entry: the literal drop-in.  The signal (or batch) is cut into chunks of about
+// kChunkElems outputs -- contiguous output ranges with a (k-1)-sample input halo, or whole
+// rows -- and three chunks are kept in flight: H2D of chunk c+1, kernels of chunk c and D2H
+// of chunk c-1 overlap on three streams, so a call costs about the slower of the two PCIe
+// directions instead of their sum.  Blocking never changes an output.
 mf_status mf_median_filter_rows(mf_context* ctx, mf_dtype dtype, const void* x, size_t rows, size_t n,
                                 size_t ld_x, size_t k, void* y, size_t ld_y) {
   if (!ctx) return MF_BAD_ARG;
@@ -202,21 +218,77 @@ mf_status mf_median_filter_rows(mf_context* ctx, mf_dtype dtype, const void* x, 
   if (keep == 0 || rows == 0) return MF_OK;
   if (!x || !y || ld_x < n || ld_y < keep) return MF_BAD_ARG;
   if (cudaSetDevice(ctx->device) != cudaSuccess) return MF_NO_DEVICE;
+  constexpr int kNumSlots = 3;
+  constexpr size_t kChunkElems = size_t(1) << 23;
+  if (!ctx->s_h2d) {
+    if (cudaStreamCreateWithFlags(&ctx->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking) != cudaSuccess)
+      return MF_CUDA_ERROR;
+    for (int i = 0; i < kNumSlots; ++i)
+      if (cudaEventCreateWithFlags(&ctx->ev_in[i], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ctx->ev_done[i], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ctx->ev_out[i], cudaEventDisableTiming) != cudaSuccess)
+        return MF_CUDA_ERROR;
+  }
   const size_t w = dtype_size(dtype);
-  const size_t in_bytes = (rows * n * w + 255) / 256 * 256;
-  const size_t out_bytes = rows * keep * w;
-  st = grow(&ctx->io, &ctx->io_bytes, in_bytes + out_bytes);
+  // chunk geometry: single signals by output ranges, batches by row groups
+  const bool by_rows = rows > 1;
+  const size_t rows_per = by_rows ? std::max<size_t>(1, kChunkElems / n) : 1;
+  const size_t out_per = by_rows ? keep : std::min(keep, std::max<size_t>(kChunkElems, 16 * k));
+  const size_t nchunks = by_rows ? (rows + rows_per - 1) / rows_per : (keep + out_per - 1) / out_per;
+  const size_t in_slot = ((by_rows ? rows_per * n : out_per + k - 1) * w + 255) / 256 * 256;
+  const size_t out_slot = ((by_rows ? rows_per * keep : out_per) * w + 255) / 256 * 256;
+  const int slots = (int)std::min<size_t>(kNumSlots, nchunks);
+  st = grow(&ctx->io, &ctx->io_bytes, slots * (in_slot + out_slot));
   if (st != MF_OK) return st;
-  char* d_x = static_cast<char*>(ctx->io);
-  char* d_y = d_x + in_bytes;
-  cudaStream_t s = ctx->stream;
-  cudaError_t e = cudaMemcpy2DAsync(d_x, n * w, x, ld_x * w, n * w, rows, cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) return from_cuda(e);
-  st = run_rows(ctx, dtype, d_x, rows, n, n, k, d_y, keep, s);
+  char* base = static_cast<char*>(ctx->io);
+  const char* hx = static_cast<const char*>(x);
+  char* hy = static_cast<char*>(y);
+  uint64_t launches = 0;
+  cudaError_t e = cudaSuccess;
+  for (size_t c = 0; c < nchunks && e == cudaSuccess; ++c) {
+    const int sl = (int)(c % slots);
+    char* d_x = base + sl * (in_slot + out_slot);
+    char* d_y = d_x + in_slot;
+    if (c >= (size_t)slots) {  // the slot's previous chunk must have left the device
+      e = cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_out[sl], 0);
+      if (e != cudaSuccess) break;
+    }
+    size_t r0 = 0, nr = 1, o0 = 0, no = keep, ni = n;
+    if (by_rows) {
+      r0 = c * rows_per;
+      nr = std::min(rows_per, rows - r0);
+      e = cudaMemcpy2DAsync(d_x, n * w, hx + r0 * ld_x * w, ld_x * w, n * w, nr, cudaMemcpyHostToDevice,
+                            ctx->s_h2d);
+    } else {
+      o0 = c * out_per;
+      no = std::min(out_per, keep - o0);
+      ni = no + k - 1;
+      e = cudaMemcpyAsync(d_x, hx + o0 * w, ni * w, cudaMemcpyHostToDevice, ctx->s_h2d);
+    }
+    if (e != cudaSuccess) break;
+    if ((e = cudaEventRecord(ctx->ev_in[sl], ctx->s_h2d)) != cudaSuccess) break;
+    if ((e = cudaStreamWaitEvent(ctx->stream, ctx->ev_in[sl], 0)) != cudaSuccess) break;
+    st = run_rows(ctx, dtype, d_x, nr, ni, ni, k, d_y, by_rows ? keep : no, ctx->stream);
+    launches += ctx->launches;
+    if (st != MF_OK) break;
+    if ((e = cudaEventRecord(ctx->ev_done[sl], ctx->stream)) != cudaSuccess) break;
+    if ((e = cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_done[sl], 0)) != cudaSuccess) break;
+    if (by_rows)
+      e = cudaMemcpy2DAsync(hy + r0 * ld_y * w, ld_y * w, d_y, keep * w, keep * w, nr, cudaMemcpyDeviceToHost,
+                            ctx->s_d2h);
+    else
+      e = cudaMemcpyAsync(hy + o0 * w, d_y, no * w, cudaMemcpyDeviceToHost, ctx->s_d2h);
+    if (e != cudaSuccess) break;
+    e = cudaEventRecord(ctx->ev_out[sl], ctx->s_d2h);
+  }
+  ctx->launches = launches;
+  const cudaError_t e2 = cudaStreamSynchronize(ctx->s_d2h);
+  const cudaError_t e3 = cudaStreamSynchronize(ctx->stream);
   if (st != MF_OK) return st;
-  e = cudaMemcpy2DAsync(y, ld_y * w, d_y, keep * w, keep * w, rows, cudaMemcpyDeviceToHost, s);
   if (e != cudaSuccess) return from_cuda(e);
-  return from_cuda(cudaStreamSynchronize(s));
+  if (e2 != cudaSuccess) return from_cuda(e2);
+  return from_cuda(e3);
 }
 
 mf_status mf_median_filter(mf_context* ctx, mf_dtype dtype, const void* x, size_t n, size_t k, void* y,
