@@ -151,9 +151,16 @@ def run_ours(args):
     import paper_1406_1717_b200 as mf
 
     world, rank, local = dist_env()
+    # one rank per GPU; MF_BENCH_BACKEND=gloo lets several ranks share a GPU for a smoke test
+    backend = os.environ.get("MF_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
+    red_dev = f"cuda:{local}" if backend == "nccl" else "cpu"
     cfg = args.config
     dtype, n, ks, gen, seed, rows = CONFIGS[cfg]
     ctx = mf.Context.get(local)
@@ -213,10 +220,10 @@ def run_ours(args):
     per_k_ms = {k: statistics.mean(a.elapsed_time(b) for a, b in ev[k]) for k in ks}
     outputs_rank = sum(nout for _k, _x, nout in jobs)
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        o = torch.tensor([outputs_rank], dtype=torch.float64, device=f"cuda:{local}")
+        o = torch.tensor([outputs_rank], dtype=torch.float64, device=red_dev)
         dist.all_reduce(o, op=dist.ReduceOp.SUM)
         outputs_total = float(o.item())
     else:
