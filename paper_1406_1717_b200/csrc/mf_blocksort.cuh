@@ -69,25 +69,39 @@ __device__ __forceinline__ void warp_sort_regs(E (&v)[R], E* s, int b0, uint32_t
   merge_levels<E, R, PS, false>(s, b0, lane, R, 32 * R, v);
 }
 
-// Load block `blk` of a row (k samples from x, +INF past n, filter.hpp:28-36) with
-// coalesced loads and warp-sort it into slot sb.  Slots beyond k hold (UMAX, e >= k),
-// which sort after everything.
-template <int DT, int R>
-__device__ __forceinline__ void warp_sort_block(Elem<typename Traits<DT>::U>* sb, const typename Traits<DT>::T* x,
-                                                uint64_t n, uint32_t k, uint64_t blk, uint32_t lane) {
-  using Tr = Traits<DT>;
-  using U = typename Tr::U;
-  using E = Elem<U>;
-  E v[R];
+// Raw (un-keyed) coalesced load of block `blk` of a row: element e = lane + 32r.  Slots
+// past k or past n (the reference's +INF padding, filter.hpp:28-36) get 0x7FF..F, whose
+// ukey is all-ones for every dtype; with index e they sort after every real element.
+template <typename TV, int R>
+__device__ __forceinline__ void warp_load_block(TV (&raw)[R], const TV* x, uint64_t n, uint32_t k, uint64_t blk,
+                                                uint32_t lane) {
+  const TV padv = (TV)(~(std::make_unsigned_t<TV>)0 >> 1);
   const uint64_t b0 = blk * k;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const uint32_t e = lane + 32 * r;
     const uint64_t gp = b0 + e;
-    const U key = (e < k && gp < n) ? Tr::enc(__ldg(x + gp)) : UMax<U>::v;
-    v[r] = E::make(key, e);
+    raw[r] = (e < k && gp < n) ? __ldg(x + gp) : padv;
   }
+}
+
+template <int DT, int R>
+__device__ __forceinline__ void warp_sort_raw(Elem<typename Traits<DT>::U>* sb, const typename Traits<DT>::T (&raw)[R],
+                                              uint32_t lane) {
+  using E = Elem<typename Traits<DT>::U>;
+  E v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) v[r] = E::make(Traits<DT>::enc(raw[r]), lane + 32 * r);
   warp_sort_regs<E, R, pad_shift<R>()>(v, sb, 0, lane);
+}
+
+// Load block `blk` of a row (k samples from x, +INF past n) and warp-sort it into slot sb.
+template <int DT, int R>
+__device__ __forceinline__ void warp_sort_block(Elem<typename Traits<DT>::U>* sb, const typename Traits<DT>::T* x,
+                                                uint64_t n, uint32_t k, uint64_t blk, uint32_t lane) {
+  typename Traits<DT>::T raw[R];
+  warp_load_block<typename Traits<DT>::T, R>(raw, x, n, k, blk, lane);
+  warp_sort_raw<DT, R>(sb, raw, lane);
 }
 
 }  // namespace mf

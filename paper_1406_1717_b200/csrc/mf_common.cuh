@@ -15,6 +15,7 @@
 // (filter.hpp:76-79), so padding never reaches an output.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace mf {

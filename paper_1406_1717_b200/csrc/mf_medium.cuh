@@ -85,6 +85,8 @@ __global__ void __launch_bounds__(32 * W) mf_medium_kernel(Geom g, uint64_t tile
   const uint64_t t_end = total_tiles * (blockIdx.x + 1) / gridDim.x;
   uint32_t base = 0;                 // physical slot of logical slot 0
   uint64_t prev_row = ~0ull, prev_tile = ~0ull;
+  TV pre[R];                         // this warp's block of the next tile, loaded during phase 2
+  bool have_pre = false;
 
   for (uint64_t t = t_begin; t < t_end; ++t) {
     const uint64_t row = t / tiles_per_row, tr = t % tiles_per_row;
@@ -97,8 +99,17 @@ __global__ void __launch_bounds__(32 * W) mf_medium_kernel(Geom g, uint64_t tile
 
     // ---------------- phase 1: warp block sorts ----------------
     if (!carry && warp == 0) warp_sort_block<DT, R>(slot(0), x, g.n, k, u0, lane);
-    warp_sort_block<DT, R>(slot(warp + 1), x, g.n, k, u0 + warp + 1, lane);
+    if (!have_pre) warp_load_block<TV, R>(pre, x, g.n, k, u0 + warp + 1, lane);
+    warp_sort_raw<DT, R>(slot(warp + 1), pre, lane);
     __syncthreads();
+    // prefetch this warp's block of the next tile; it lands while phase 2 runs (large
+    // blocks only: for small R the extra registers cost more occupancy than they hide)
+    have_pre = R >= 16 && t + 1 < t_end;
+    if (have_pre) {
+      const uint64_t nrow = (t + 1) / tiles_per_row, ntr = (t + 1) % tiles_per_row;
+      warp_load_block<TV, R>(pre, reinterpret_cast<const TV*>(g.x) + nrow * g.ld_x, g.n, k, ntr * W + warp + 1,
+                             lane);
+    }
 
     // ---------------- phase 2: per-pair postprocess ----------------
     const uint64_t u = u0 + warp;
@@ -112,38 +123,50 @@ __global__ void __launch_bounds__(32 * W) mf_medium_kernel(Geom g, uint64_t tile
       for (uint32_t w = lane; w < NW; w += 32) abits[w] = 0;
       __syncwarp();
 
-      // merge path: lane owns merged positions [lane*2R, lane*2R + 2R)
+      // merge path: lane owns merged positions [lane*2R, lane*2R + 2R); branch-free steps
       {
         const int d = lane * 2 * R;
-        if ((uint32_t)d < nq) {
-          const int K = (int)k;
-          int lo = d > K ? d - K : 0, hi = d < K ? d : K;
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (A[pad<PS>(mid)].key() <= B[pad<PS>(d - 1 - mid)].key()) lo = mid + 1; else hi = mid;
-          }
-          int ia = lo, ib = d - lo;
-          E ea = A[pad<PS>(min(ia, K - 1))], eb = B[pad<PS>(min(ib, K - 1))];
+        const int K = (int)k;
+        int lo = d > K ? d - K : 0, hi = d < K ? d : K;
+        if (d >= (int)nq) lo = hi = 0;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (A[pad<PS>(mid)].key() <= B[pad<PS>(d - 1 - mid)].key()) lo = mid + 1; else hi = mid;
+        }
+        int ia = lo, ib = d - lo;
+        E ea = A[pad<PS>(min(ia, K - 1))], eb = B[pad<PS>(min(max(ib, 0), K - 1))];
+        uint64_t amask = 0;                      // A-side bits of this lane's 2R positions
+        uint16_t* rab16 = reinterpret_cast<uint16_t*>(rab);
 #pragma unroll 4
-          for (int r = 0; r < 2 * R; ++r) {
-            const int q = d + r;
-            if (q >= (int)nq) break;
-            const bool takeA = (ib >= K) || (ia < K && ea.key() <= eb.key());
-            const uint32_t idx = takeA ? ea.idx() : eb.idx();
-            const uint32_t c = idx / R;            // owning lane (chunk) of this element
+        for (int r = 0; r < 2 * R; ++r) {
+          const int q = d + r;
+          const bool valid = q < (int)nq;
+          const bool takeA = (ib >= K) || (ia < K && ea.key() <= eb.key());
+          const uint32_t idx = sel(takeA, ea.idx(), eb.idx());
+          const uint32_t c = idx / R;            // owning lane (chunk) of this element
+          if (valid) {
             atomicOr(&rows[row_addr(c, q >> 5)], 1u << (q & 31));
-            if (takeA) {
-              src[q] = (uint16_t)ia;
-              atomicOr(&abits[q >> 5], 1u << (q & 31));
-              reinterpret_cast<uint16_t*>(rab)[2 * ((idx % R) * 32 + c)] = (uint16_t)q;
-              ++ia;
-              ea = A[pad<PS>(min(ia, K - 1))];
-            } else {
-              src[q] = (uint16_t)(0x8000u | ib);
-              reinterpret_cast<uint16_t*>(rab)[2 * ((idx % R) * 32 + c) + 1] = (uint16_t)q;
-              ++ib;
-              eb = B[pad<PS>(min(ib, K - 1))];
-            }
+            src[q] = (uint16_t)sel(takeA, (uint32_t)ia, 0x8000u | (uint32_t)ib);
+            rab16[2 * ((idx % R) * 32 + c) + (takeA ? 0 : 1)] = (uint16_t)q;
+          }
+          amask |= (uint64_t)(valid && takeA) << r;
+          ia += takeA;
+          ib += !takeA;
+          const E nv = takeA ? A[pad<PS>(min(ia, K - 1))] : B[pad<PS>(min(ib, K - 1))];
+          ea = E::select(takeA, nv, ea);
+          eb = E::select(takeA, eb, nv);
+        }
+        // fold the lane's A bits into abits (2R <= 64 positions, at most 3 words)
+        if (d < (int)nq) {
+#pragma unroll
+          for (int w0 = 0; w0 < (2 * R + 31) / 32 + 1; ++w0) {
+            const int wq = (d >> 5) + w0;
+            const int sh = wq * 32 - d;          // bit offset of word wq in amask
+            uint32_t bits;
+            if (sh >= 64 || sh <= -32) bits = 0;
+            else if (sh >= 0) bits = (uint32_t)(amask >> sh);
+            else bits = (uint32_t)(amask << (-sh));
+            if (bits) atomicOr(&abits[wq], bits);
           }
         }
       }

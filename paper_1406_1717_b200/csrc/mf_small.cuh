@@ -84,7 +84,7 @@ __device__ __forceinline__ int misalign(const TV* p) {
 template <typename TV, int NE, int T>
 __device__ __forceinline__ void stage_tile(TV* buf, const TV* x, uint64_t n, uint64_t base) {
   constexpr int EPC = 16 / (int)sizeof(TV);  // elements per 16-byte chunk
-  const TV pad = (TV)(~(TV)0 >> 1);
+  const TV pad = (TV)(~(std::make_unsigned_t<TV>)0 >> 1);
   const int mis = misalign(x + base);
   TV* dst = buf + mis;
   const TV* src = x + base;
