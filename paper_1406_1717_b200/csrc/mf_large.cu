@@ -29,6 +29,8 @@ LargeGeom plan(const Geom& g, uint64_t nb) {
   while (cl < 1024 && (g.k + cl - 1) / cl > 256) cl *= 2;
   while ((g.k + cl - 1) / cl > 4096) cl *= 2;  // bounds the per-CTA histogram (8C words)
   L.CL = cl;
+  L.CLshift = 0;
+  while ((1u << L.CLshift) < cl) ++L.CLshift;
   L.C = (g.k + cl - 1) / cl;
   L.NS = (L.nq + 1023) / 1024;
   return L;
@@ -46,6 +48,9 @@ cudaError_t configure(const LargeGeom& L) {
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(ml_merge_pass<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)merge_tile_smem<U>());
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(ml_walk<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(U) * 32 * 9 * (LNT / 32)));
     if (e != cudaSuccess) return e;
     done = true;
   }
@@ -72,7 +77,7 @@ struct Layout {
     if (!sort_only) {
       off_mk = o; o = align_up(o + sizeof(U) * nu * L.nqp, 256);
       off_org = o; o = align_up(o + sizeof(uint32_t) * nu * L.nqp, 256);
-      off_rab = o; o = align_up(o + sizeof(uint2) * nu * L.g.k, 256);
+      off_rab = o; o = align_up(o + sizeof(uint2) * nu * L.C * L.CL, 256);
       off_live = o; o = align_up(o + sizeof(uint32_t) * nu * L.C * L.NS, 256);
     }
     total = o;
@@ -120,9 +125,8 @@ cudaError_t run_large_dt(const Geom& g, void* wsv, size_t ws_bytes, cudaStream_t
   ml_unit_merge<DT><<<dim3((unsigned)(g.units * L.tiles2), g.rows), LNT, um, s>>>(L, sorted, mk, org, rab, live);
   ++*launches;
   const uint64_t nchunks = nu * L.C;
-  ml_scan<<<(unsigned)((nchunks + LNT - 1) / LNT), LNT, 0, s>>>(L, live, nchunks);
-  ++*launches;
-  ml_walk<DT><<<(unsigned)((nchunks + LNT - 1) / LNT), LNT, 0, s>>>(L, mk, org, rab, live, nchunks);
+  ml_walk<DT><<<(unsigned)((nchunks + LNT - 1) / LNT), LNT, sizeof(U) * 32 * 9 * (LNT / 32), s>>>(
+      L, mk, org, rab, live, nchunks);
   ++*launches;
   return cudaGetLastError();
 }

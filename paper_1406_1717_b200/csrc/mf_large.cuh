@@ -12,7 +12,6 @@
 //                     merged-position -> (block, index), index -> merged position
 //                     (the Delete(A,i) / Undelete(B,i) targets), and, fused, the live
 //                     counts of every 1024-position "superword" at every chunk start;
-//     ml_scan         prefix of those counts: the selection index for a chunk's first median;
 //     ml_walk         one thread per chunk of CL steps.  The state before step i is the
 //                     live set {A: idx >= i} u {B: idx < i} (Eq. 4 / Lemma 1,
 //                     SURVEY.md §0.6); the thread keeps only the cursor p and the one
@@ -53,7 +52,8 @@ struct LargeGeom {
   uint32_t nq;        // merged positions per unit = 2k
   uint32_t nqp;       // padded stride (multiple of 32)
   uint32_t tiles2;    // unit-merge tiles per unit = ceil(2k / LQ)
-  uint32_t CL;        // steps per walk chunk
+  uint32_t CL;        // steps per walk chunk (a power of two)
+  uint32_t CLshift;   // log2(CL)
   uint32_t C;         // chunks per unit
   uint32_t NS;        // superwords (1024 positions) per unit
 };
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(LNT) ml_unit_merge(LargeGeom L, const Elem<typ
   uint32_t nx;
   const int cnt = merge_tile(s, A, k, B, k, d0, d1, before, v, srcB, split, nx);
   const int dd = threadIdx.x * LR2;
-  uint2* ro = rab + ug * k;
+  uint2* ro = rab + ug * (uint64_t)L.C * L.CL;
   __syncthreads();
   U* sk = reinterpret_cast<U*>(s);                          // staging: keys, then origins
   uint32_t* so = reinterpret_cast<uint32_t*>(sk + LQ);
@@ -233,7 +233,8 @@ __global__ void __launch_bounds__(LNT) ml_unit_merge(LargeGeom L, const Elem<typ
       const uint32_t idx = v[r].idx();
       sk[dd + r] = v[r].key();
       so[dd + r] = idx | (srcB[r] ? 0x80000000u : 0u);
-      if (srcB[r]) ro[idx].y = q; else ro[idx].x = q;
+      uint2* slot = ro + (uint64_t)(idx & (L.CL - 1)) * C + (idx >> L.CLshift);  // transposed [t][c]
+      if (srcB[r]) slot->y = q; else slot->x = q;
       const uint32_t sw = (dd + r) >> 10;                   // superword within the tile
       atomicAdd(&hist[(sw * 2 + (srcB[r] ? 1 : 0)) * C + idx / L.CL], 1u);
     }
@@ -269,17 +270,6 @@ __global__ void __launch_bounds__(LNT) ml_unit_merge(LargeGeom L, const Elem<typ
   }
 }
 
-// exclusive prefix over superwords of the live counts, per (unit, chunk)
-__global__ void ml_scan(LargeGeom L, uint32_t* live, uint64_t total) {
-  const uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= total) return;
-  const uint64_t ug = id / L.C;
-  const uint32_t c = id % L.C;
-  uint32_t* p = live + ug * L.NS * L.C + c;
-  uint32_t acc = 0;
-  for (uint32_t S = 0; S < L.NS; ++S) { const uint32_t t = p[S * L.C]; p[S * L.C] = acc; acc += t; }
-}
-
 // live bits of merged positions [32w, 32w+32) just before step i (output i)
 __device__ __forceinline__ uint32_t live_word(const uint32_t* og, uint32_t w, uint32_t i, uint32_t nq) {
   uint32_t bits = 0;
@@ -301,64 +291,113 @@ __device__ __forceinline__ uint32_t live_word(const uint32_t* og, uint32_t w, ui
 }
 
 // ---- phase 2c: chunked walk -----------------------------------------------------------
+// Thread id = ug*C + c walks chunk c of unit ug: outputs [c*CL, c*CL + CL).  Consecutive
+// lanes take consecutive chunks, so the per-step Delete/Undelete targets (stored
+// transposed, rab[t*C + c]) are read coalesced; outputs are gathered 8 steps at a time
+// in shared memory and written back as 32-byte runs, four chunks per warp store.
 template <int DT>
 __global__ void __launch_bounds__(LNT) ml_walk(LargeGeom L, const typename Traits<DT>::U* mk, const uint32_t* org,
                                                const uint2* rab, const uint32_t* live, uint64_t total) {
   using Tr = Traits<DT>;
   using U = typename Tr::U;
   using TV = typename Tr::T;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  U* stage = reinterpret_cast<U*>(smem_raw) + warp * 32 * 9;    // [lane][step] with stride 9
   const uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= total) return;
-  const uint64_t ug = id / L.C;
-  const uint32_t c = id % L.C;
   const Geom& g = L.g;
-  const uint64_t row = ug / g.units, u = ug % g.units;
   const uint32_t k = g.k, h = g.h;
-  const uint64_t rem = g.keep - u * k;
-  const uint32_t imax = rem < (uint64_t)k ? (uint32_t)rem : k;
-  const uint32_t i0 = c * L.CL;
-  if (i0 >= imax) return;
-  const uint32_t i1 = min(imax, i0 + L.CL);
+  uint64_t ug = 0, row = 0, u = 0;
+  uint32_t c = 0, i0 = 0, i1 = 0;
+  if (id < total) {
+    ug = id / L.C;
+    c = id % L.C;
+    row = ug / g.units;
+    u = ug % g.units;
+    const uint64_t rem = g.keep - u * k;
+    const uint32_t imax = rem < (uint64_t)k ? (uint32_t)rem : k;
+    i0 = c * L.CL;
+    i1 = min(imax, i0 + L.CL);
+    if (i0 > i1) i0 = i1;
+  }
+  const bool active = i0 < i1;
   const uint32_t* og = org + ug * L.nqp;
   const U* mkg = mk + ug * L.nqp;
-  const uint2* rb = rab + ug * k;
-  const uint32_t* cum = live + ug * L.NS * L.C + c;   // stride C over superwords
-  TV* y = reinterpret_cast<TV*>(g.y) + row * g.ld_y + u * k;
+  const uint2* rb = rab + ug * (uint64_t)L.C * L.CL + c;      // step t at rb[t * C]
+  TV* y = reinterpret_cast<TV*>(g.y) + row * g.ld_y + u * k + i0;
 
-  // select: superword with cum[S] <= h < cum[S+1], then words inside it
-  uint32_t lo = 0, hi = L.NS - 1;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi + 1) >> 1;
-    if (__ldg(cum + mid * L.C) <= h) lo = mid; else hi = mid - 1;
-  }
-  uint32_t r = h - __ldg(cum + lo * L.C);
-  uint32_t cw = lo * 32, cb = 0;
-  for (;; ++cw) {
-    cb = live_word(og, cw, i0, L.nq);
-    const uint32_t pc = __popc(cb);
-    if (r < pc) break;
-    r -= pc;
-  }
-  uint32_t p = cw * 32 + __fns(cb, 0, (int)r + 1);
-  y[i0] = Tr::dec(mkg[p]);
-  for (uint32_t i = i0 + 1; i < i1; ++i) {
-    const uint2 ab = __ldg(rb + i - 1);
-    const uint32_t a = ab.x, b = ab.y;
-    if ((a >> 5) == cw) cb &= ~(1u << (a & 31));
-    if ((b >> 5) == cw) cb |= 1u << (b & 31);
-    const bool up = (a == p) ? (b > p) : (a < p && b > p);
-    const bool down = (a == p) ? (b < p) : (a > p && b < p);
-    if (up) {
-      const uint32_t sh = (p & 31) + 1;
-      uint32_t m = sh < 32 ? cb & (0xFFFFFFFFu << sh) : 0;
-      while (m == 0) { ++cw; cb = live_word(og, cw, i, L.nq); m = cb; }
-      p = cw * 32 + __ffs(m) - 1;
-    } else if (down) {
-      uint32_t m = cb & ((1u << (p & 31)) - 1u);
-      while (m == 0) { --cw; cb = live_word(og, cw, i, L.nq); m = cb; }
-      p = cw * 32 + 31 - __clz(m);
+  uint32_t p = 0, cw = 0, cb = 0;
+  if (active) {
+    // select: superword S with prefix(S) <= h < prefix(S+1) (prefix of the live counts,
+    // read 8 superwords at a time), then the words inside it
+    const uint32_t* cnt = live + ug * L.NS * L.C + c;          // stride C over superwords
+    uint32_t acc = 0, S = 0;
+    for (; S < L.NS; S += 8) {
+      uint32_t v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = S + j < L.NS ? __ldg(cnt + (uint64_t)(S + j) * L.C) : 0xFFFFFFFFu;
+      uint32_t s8 = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s8 += (S + j < L.NS) ? v[j] : 0;
+      if (acc + s8 > h) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (acc + v[j] > h) { S += j; break; }
+          acc += v[j];
+        }
+        break;
+      }
+      acc += s8;
     }
-    y[i] = Tr::dec(mkg[p]);
+    uint32_t r = h - acc;
+    cw = S * 32;
+    for (;; ++cw) {
+      cb = live_word(og, cw, i0, L.nq);
+      const uint32_t pc = __popc(cb);
+      if (r < pc) break;
+      r -= pc;
+    }
+    p = cw * 32 + __fns(cb, 0, (int)r + 1);
+  }
+  const uint32_t my_n = active ? i1 - i0 : 0u;
+  for (uint32_t t0 = 0; t0 < L.CL; t0 += 8) {
+#pragma unroll 2
+    for (uint32_t tt = 0; tt < 8; ++tt) {
+      const uint32_t t = t0 + tt;
+      const uint32_t i = i0 + t;
+      if (t < my_n) {
+        if (t > 0) {
+          const uint2 ab = __ldg(rb + (uint64_t)(t - 1) * L.C);
+          const uint32_t a = ab.x, b = ab.y;
+          if ((a >> 5) == cw) cb &= ~(1u << (a & 31));
+          if ((b >> 5) == cw) cb |= 1u << (b & 31);
+          const bool up = (a == p) ? (b > p) : (a < p && b > p);
+          const bool down = (a == p) ? (b < p) : (a > p && b < p);
+          if (up) {
+            const uint32_t sh = (p & 31) + 1;
+            uint32_t m = sh < 32 ? cb & (0xFFFFFFFFu << sh) : 0;
+            while (m == 0) { ++cw; cb = live_word(og, cw, i, L.nq); m = cb; }
+            p = cw * 32 + __ffs(m) - 1;
+          } else if (down) {
+            uint32_t m = cb & ((1u << (p & 31)) - 1u);
+            while (m == 0) { --cw; cb = live_word(og, cw, i, L.nq); m = cb; }
+            p = cw * 32 + 31 - __clz(m);
+          }
+        }
+        stage[lane * 9 + tt] = __ldg(mkg + p);
+      }
+    }
+    __syncwarp();
+    // 8 outputs of 4 chunks per warp store: lane l -> chunk 4j + l/8, step l%8
+#pragma unroll
+    for (uint32_t j = 0; j < 8; ++j) {
+      const uint32_t src = 4 * j + (lane >> 3), st = lane & 7;
+      const uint32_t jn = __shfl_sync(0xFFFFFFFFu, my_n, src);
+      TV* yj = reinterpret_cast<TV*>(__shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(y), src));
+      if (t0 + st < jn) yj[t0 + st] = Tr::dec(stage[src * 9 + st]);
+    }
+    __syncwarp();
+    if (__all_sync(0xFFFFFFFFu, t0 + 8 >= my_n)) break;
   }
 }
 
