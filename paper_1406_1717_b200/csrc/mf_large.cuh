@@ -60,7 +60,7 @@ struct LargeGeom {
 
 // ---- phase 1a: sort TS-element tiles of every block ----------------------------------
 template <int DT>
-__global__ void __launch_bounds__(LNT) ml_tile_sort(LargeGeom L, Elem<typename Traits<DT>::U>* out) {
+__global__ void __launch_bounds__(LNT, 3) ml_tile_sort(LargeGeom L, Elem<typename Traits<DT>::U>* out) {
   using Tr = Traits<DT>;
   using U = typename Tr::U;
   using E = Elem<U>;
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(LNT) ml_merge_pass(LargeGeom L, const Elem<typ
 
 // ---- phase 2a: merge each pair (A = block u, B = block u+1) + live counts -------------
 template <int DT>
-__global__ void __launch_bounds__(LNT) ml_unit_merge(LargeGeom L, const Elem<typename Traits<DT>::U>* S,
+__global__ void __launch_bounds__(LNT, 4) ml_unit_merge(LargeGeom L, const Elem<typename Traits<DT>::U>* S,
                                                      typename Traits<DT>::U* mk, uint32_t* org, uint2* rab,
                                                      uint32_t* live) {
   using U = typename Traits<DT>::U;
