@@ -23,8 +23,18 @@ constexpr int pad_shift() { return R >= 32 ? 5 : 4; }
 // multiple of R) inside s[b0 .. b0 + NT*R), NT threads, thread `tid` produces the R
 // outputs [tid*R, tid*R + R) of its merged pair.  On entry s holds sorted runs of
 // length run0; v is scratch.  CTA = true syncs the CTA, else the warp.
-template <typename E, int R, int PS, bool CTA>
-__device__ __forceinline__ void merge_levels(E* s, int b0, int tid, int run0, int run_end, E (&v)[R]) {
+struct SyncWarp { __device__ __forceinline__ void operator()() const { __syncwarp(); } };
+struct SyncCta { __device__ __forceinline__ void operator()() const { __syncthreads(); } };
+// named barrier over `count` threads (a team of warps), id != 0
+struct SyncTeam {
+  uint32_t id, count;
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+  }
+};
+
+template <typename E, int R, int PS, typename Sync>
+__device__ __forceinline__ void merge_levels_s(E* s, int b0, int tid, int run0, int run_end, E (&v)[R], Sync sync) {
 #pragma unroll 1
   for (int run = run0; run < run_end; run *= 2) {
     const int gl = (2 * run) / R;                // threads per merged run
@@ -51,11 +61,17 @@ __device__ __forceinline__ void merge_levels(E* s, int b0, int tid, int run0, in
       xa = E::select(takeA, nv, xa);
       yv = E::select(takeA, yv, nv);
     }
-    if (CTA) __syncthreads(); else __syncwarp();
+    sync();
 #pragma unroll
     for (int r = 0; r < R; ++r) s[pad<PS>(xb + d + r)] = v[r];
-    if (CTA) __syncthreads(); else __syncwarp();
+    sync();
   }
+}
+
+template <typename E, int R, int PS, bool CTA>
+__device__ __forceinline__ void merge_levels(E* s, int b0, int tid, int run0, int run_end, E (&v)[R]) {
+  if constexpr (CTA) merge_levels_s<E, R, PS>(s, b0, tid, run0, run_end, v, SyncCta{});
+  else merge_levels_s<E, R, PS>(s, b0, tid, run0, run_end, v, SyncWarp{});
 }
 
 // Warp sort of 32*R register-loaded elements (v, any distribution over lanes) into
@@ -93,6 +109,37 @@ __device__ __forceinline__ void warp_sort_raw(Elem<typename Traits<DT>::U>* sb, 
 #pragma unroll
   for (int r = 0; r < R; ++r) v[r] = E::make(Traits<DT>::enc(raw[r]), lane + 32 * r);
   warp_sort_regs<E, R, pad_shift<R>()>(v, sb, 0, lane);
+}
+
+// Team sort: WP warps sort one block of 32*RS*WP slots.  Warp `sub` of the team holds the
+// elements [sub*32*RS, (sub+1)*32*RS) (element e = sub*32*RS + lane + 32r), sorts them
+// into its part of sb, then the team merges the WP sorted parts.
+template <int DT, int RS, int WP>
+__device__ __forceinline__ void team_sort_raw(Elem<typename Traits<DT>::U>* sb, const typename Traits<DT>::T (&raw)[RS],
+                                              uint32_t sub, uint32_t lane, SyncTeam bar) {
+  using E = Elem<typename Traits<DT>::U>;
+  constexpr int PS = pad_shift<RS>();
+  E v[RS];
+#pragma unroll
+  for (int r = 0; r < RS; ++r) v[r] = E::make(Traits<DT>::enc(raw[r]), sub * 32 * RS + lane + 32 * r);
+  warp_sort_regs<E, RS, PS>(v, sb, sub * 32 * RS, lane);
+  if constexpr (WP > 1) {
+    bar();
+    merge_levels_s<E, RS, PS>(sb, 0, sub * 32 + lane, 32 * RS, 32 * RS * WP, v, bar);
+  }
+}
+
+template <typename TV, int RS, int WP>
+__device__ __forceinline__ void team_load_block(TV (&raw)[RS], const TV* x, uint64_t n, uint32_t k, uint64_t blk,
+                                                uint32_t sub, uint32_t lane) {
+  const TV padv = (TV)(~(std::make_unsigned_t<TV>)0 >> 1);
+  const uint64_t b0 = blk * k;
+#pragma unroll
+  for (int r = 0; r < RS; ++r) {
+    const uint32_t e = sub * 32 * RS + lane + 32 * r;
+    const uint64_t gp = b0 + e;
+    raw[r] = (e < k && gp < n) ? __ldg(x + gp) : padv;
+  }
 }
 
 // Load block `blk` of a row (k samples from x, +INF past n) and warp-sort it into slot sb.

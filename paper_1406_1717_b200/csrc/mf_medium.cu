@@ -16,8 +16,9 @@ template <int DT, int R> struct WarpsFor {
 template <int DT, int R>
 cudaError_t launch_r(const Geom& g, cudaStream_t s) {
   constexpr int W = WarpsFor<DT, R>::value;
-  using C = MediumCfg<DT, R, W>;
-  auto kern = mf_medium_kernel<DT, R, W>;
+  constexpr int WP = 1;  // warps per block pair (team); 2 measured slower at k=1023 (register-bound)
+  using C = MediumCfg<DT, R, W, WP>;
+  auto kern = mf_medium_kernel<DT, R, W, WP>;
   static int resident = 0;  // CTAs per SM (per process; the attribute is idempotent)
   static int sms = 0;
   if (!resident) {
@@ -26,7 +27,7 @@ cudaError_t launch_r(const Geom& g, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, 32 * W, C::smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, 32 * W * WP, C::smem);
     if (e != cudaSuccess) return e;
     if (resident < 1) resident = 1;
   }
@@ -34,7 +35,7 @@ cudaError_t launch_r(const Geom& g, cudaStream_t s) {
   const uint64_t total = tiles_per_row * g.rows;
   // persistent grid: each CTA walks a contiguous range of tiles (ring-carried blocks)
   const uint64_t ctas = std::min<uint64_t>(total, (uint64_t)sms * resident);
-  kern<<<(unsigned)ctas, 32 * W, C::smem, s>>>(g, tiles_per_row, total);
+  kern<<<(unsigned)ctas, 32 * W * WP, C::smem, s>>>(g, tiles_per_row, total);
   return cudaGetLastError();
 }
 

@@ -34,15 +34,16 @@
 
 namespace mf {
 
-template <int DT, int R, int W>
+template <int DT, int R, int W, int WP = 1>
 struct MediumCfg {
   using Tr = Traits<DT>;
   using U = typename Tr::U;
   using E = Elem<U>;
   static constexpr int BS = 32 * R;        // block slot capacity (>= k)
   static constexpr int NW = 2 * R;         // words per merged row (2k bits <= 64R)
+  static constexpr int RS = R / WP;        // elements per lane in the team block sort
   // padded element index: blocked per-lane writes hit distinct banks (8-byte elements)
-  static constexpr int PS = pad_shift<R>();
+  static constexpr int PS = pad_shift<RS>();
   static constexpr int SLOT = BS + (BS >> PS) + 1;
   static constexpr size_t sz_sorted = sizeof(E) * SLOT * (W + 1);
   static constexpr size_t sz_src = sizeof(uint16_t) * 2 * BS;  // merged pos -> (isB, sorted pos)
@@ -52,7 +53,7 @@ struct MediumCfg {
   // the rows area doubles as the output staging area after the walk
   static constexpr size_t sz_rows = (sz_rows_bits > sz_stage ? sz_rows_bits : sz_stage + 15) / 16 * 16;
   static constexpr size_t sz_abits = sizeof(uint32_t) * NW;
-  static constexpr size_t sz_warp = (sz_src + sz_rab + sz_rows + sz_abits + 15) / 16 * 16;
+  static constexpr size_t sz_warp = (sz_src + sz_rab + sz_rows + sz_abits + 15) / 16 * 16;  // per team
   static constexpr size_t smem = sz_sorted + W * sz_warp;
 };
 
@@ -60,18 +61,26 @@ struct MediumCfg {
 // over L) and the walk (lane = L, data-dependent word) are both bank-spread.
 __device__ __forceinline__ uint32_t row_addr(uint32_t L, uint32_t w) { return w * 32 + (L ^ (w & 31)); }
 
-template <int DT, int R, int W>
-__global__ void __launch_bounds__(32 * W) mf_medium_kernel(Geom g, uint64_t tiles_per_row, uint64_t total_tiles) {
-  using C = MediumCfg<DT, R, W>;
+// A "team" of WP warps owns one block pair: it sorts the pair's B block together (WP warp
+// sorts + a team merge level), runs the pair merge and the XOR prefix with 32*WP lanes,
+// and its first warp walks the 32 chunks.  WP = 2 for the largest blocks halves the
+// dependent merge chains that bound them at low occupancy.
+template <int DT, int R, int W, int WP>
+__global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t tiles_per_row, uint64_t total_tiles) {
+  using C = MediumCfg<DT, R, W, WP>;
   using Tr = typename C::Tr;
   using U = typename C::U;
   using E = typename C::E;
   using TV = typename Tr::T;
-  constexpr int NW = C::NW, PS = C::PS, SLOT = C::SLOT;
+  constexpr int NW = C::NW, PS = C::PS, SLOT = C::SLOT, RS = C::RS;
+  constexpr int TL = 32 * WP;        // team lanes
   extern __shared__ __align__(16) unsigned char smem[];
   E* ring = reinterpret_cast<E*>(smem);
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* ws = smem + C::sz_sorted + warp * C::sz_warp;
+  const uint32_t team = warp / WP, sub = warp % WP, tl = sub * 32 + lane;
+  const SyncTeam tbar{1 + team, (uint32_t)TL};
+  auto team_sync = [&]() { if constexpr (WP > 1) tbar(); else __syncwarp(); };
+  unsigned char* ws = smem + C::sz_sorted + team * C::sz_warp;
   uint16_t* src = reinterpret_cast<uint16_t*>(ws);
   uint32_t* rab = reinterpret_cast<uint32_t*>(ws + C::sz_src);
   uint32_t* rows = reinterpret_cast<uint32_t*>(ws + C::sz_src + C::sz_rab);
@@ -85,7 +94,7 @@ __global__ void __launch_bounds__(32 * W) mf_medium_kernel(Geom g, uint64_t tile
   const uint64_t t_end = total_tiles * (blockIdx.x + 1) / gridDim.x;
   uint32_t base = 0;                 // physical slot of logical slot 0
   uint64_t prev_row = ~0ull, prev_tile = ~0ull;
-  TV pre[R];                         // this warp's block of the next tile, loaded during phase 2
+  TV pre[RS];                        // this lane's part of the team's next block, loaded during phase 2
   bool have_pre = false;
 
   for (uint64_t t = t_begin; t < t_end; ++t) {
@@ -97,35 +106,40 @@ __global__ void __launch_bounds__(32 * W) mf_medium_kernel(Geom g, uint64_t tile
     if (carry) base = (base + W) % (W + 1);
     auto slot = [&](uint32_t logical) { return ring + ((base + logical) % (W + 1)) * SLOT; };
 
-    // ---------------- phase 1: warp block sorts ----------------
-    if (!carry && warp == 0) warp_sort_block<DT, R>(slot(0), x, g.n, k, u0, lane);
-    if (!have_pre) warp_load_block<TV, R>(pre, x, g.n, k, u0 + warp + 1, lane);
-    warp_sort_raw<DT, R>(slot(warp + 1), pre, lane);
+    // ---------------- phase 1: team block sorts ----------------
+    if (!carry && team == 0) {
+      TV raw0[RS];
+      team_load_block<TV, RS, WP>(raw0, x, g.n, k, u0, sub, lane);
+      team_sort_raw<DT, RS, WP>(slot(0), raw0, sub, lane, tbar);
+    }
+    if (!have_pre) team_load_block<TV, RS, WP>(pre, x, g.n, k, u0 + team + 1, sub, lane);
+    team_sort_raw<DT, RS, WP>(slot(team + 1), pre, sub, lane, tbar);
     __syncthreads();
-    // prefetch this warp's block of the next tile; it lands while phase 2 runs (large
+    // prefetch this team's block of the next tile; it lands while phase 2 runs (large
     // blocks only: for small R the extra registers cost more occupancy than they hide)
     have_pre = R >= 16 && t + 1 < t_end;
     if (have_pre) {
       const uint64_t nrow = (t + 1) / tiles_per_row, ntr = (t + 1) % tiles_per_row;
-      warp_load_block<TV, R>(pre, reinterpret_cast<const TV*>(g.x) + nrow * g.ld_x, g.n, k, ntr * W + warp + 1,
-                             lane);
+      team_load_block<TV, RS, WP>(pre, reinterpret_cast<const TV*>(g.x) + nrow * g.ld_x, g.n, k,
+                                  ntr * W + team + 1, sub, lane);
     }
 
     // ---------------- phase 2: per-pair postprocess ----------------
-    const uint64_t u = u0 + warp;
+    const uint64_t u = u0 + team;
     if (u < g.units) {
       const uint64_t rem = g.keep - u * k;
       const uint32_t imax = rem < (uint64_t)k ? (uint32_t)rem : k;
-      const E* A = slot(warp);
-      const E* B = slot(warp + 1);
+      const E* A = slot(team);
+      const E* B = slot(team + 1);
 
-      for (uint32_t i = lane; i < NW * 32; i += 32) rows[i] = 0;
-      for (uint32_t w = lane; w < NW; w += 32) abits[w] = 0;
-      __syncwarp();
+      for (uint32_t i = tl; i < NW * 32; i += TL) rows[i] = 0;
+      for (uint32_t w = tl; w < NW; w += TL) abits[w] = 0;
+      team_sync();
 
-      // merge path: lane owns merged positions [lane*2R, lane*2R + 2R); branch-free steps
+      // merge path: team lane owns merged positions [tl*PL, tl*PL + PL); branch-free steps
       {
-        const int d = lane * 2 * R;
+        constexpr int PL = 2 * R / WP;
+        const int d = tl * PL;
         const int K = (int)k;
         int lo = d > K ? d - K : 0, hi = d < K ? d : K;
         if (d >= (int)nq) lo = hi = 0;
@@ -135,10 +149,10 @@ __global__ void __launch_bounds__(32 * W) mf_medium_kernel(Geom g, uint64_t tile
         }
         int ia = lo, ib = d - lo;
         E ea = A[pad<PS>(min(ia, K - 1))], eb = B[pad<PS>(min(max(ib, 0), K - 1))];
-        uint64_t amask = 0;                      // A-side bits of this lane's 2R positions
+        uint64_t amask = 0;                      // A-side bits of this lane's PL positions
         uint16_t* rab16 = reinterpret_cast<uint16_t*>(rab);
 #pragma unroll 4
-        for (int r = 0; r < 2 * R; ++r) {
+        for (int r = 0; r < PL; ++r) {
           const int q = d + r;
           const bool valid = q < (int)nq;
           const bool takeA = (ib >= K) || (ia < K && ea.key() <= eb.key());
@@ -156,10 +170,10 @@ __global__ void __launch_bounds__(32 * W) mf_medium_kernel(Geom g, uint64_t tile
           ea = E::select(takeA, nv, ea);
           eb = E::select(takeA, eb, nv);
         }
-        // fold the lane's A bits into abits (2R <= 64 positions, at most 3 words)
+        // fold the lane's A bits into abits (PL <= 64 positions, at most 3 words)
         if (d < (int)nq) {
 #pragma unroll
-          for (int w0 = 0; w0 < (2 * R + 31) / 32 + 1; ++w0) {
+          for (int w0 = 0; w0 < (PL + 31) / 32 + 1; ++w0) {
             const int wq = (d >> 5) + w0;
             const int sh = wq * 32 - d;          // bit offset of word wq in amask
             uint32_t bits;
@@ -170,9 +184,9 @@ __global__ void __launch_bounds__(32 * W) mf_medium_kernel(Geom g, uint64_t tile
           }
         }
       }
-      __syncwarp();
+      team_sync();
       // XOR prefix over chunks: row_L = A_bits ^ (toggles of chunks < L)
-      for (uint32_t w = lane; w < nw; w += 32) {
+      for (uint32_t w = tl; w < nw; w += TL) {
         uint32_t acc = abits[w];
 #pragma unroll 8
         for (uint32_t L = 0; L < 32; ++L) {
@@ -182,59 +196,61 @@ __global__ void __launch_bounds__(32 * W) mf_medium_kernel(Geom g, uint64_t tile
           acc ^= dlt;
         }
       }
-      __syncwarp();
+      team_sync();
 
-      auto key_at = [&](uint32_t p) -> U {
-        const uint32_t s = src[p];
-        return (s & 0x8000u) ? B[pad<PS>(s & 0x7FFF)].key() : A[pad<PS>(s)].key();
-      };
+      if (sub == 0) {
+        auto key_at = [&](uint32_t p) -> U {
+          const uint32_t s = src[p];
+          return (s & 0x8000u) ? B[pad<PS>(s & 0x7FFF)].key() : A[pad<PS>(s)].key();
+        };
 
-      // walk: lane L emits outputs [L*R, L*R + R) of this unit
-      const uint32_t i0 = lane * R;
-      U out[R];
-      if (i0 < imax) {
-        // select the (h+1)-th live position of row_L
-        uint32_t cnt = 0, cw = 0, cb = 0;
-        for (;; ++cw) {
-          cb = rows[row_addr(lane, cw)];
-          const uint32_t pc = __popc(cb);
-          if (cnt + pc > h) break;
-          cnt += pc;
-        }
-        uint32_t p = cw * 32 + __fns(cb, 0, (int)(h - cnt) + 1);
-        out[0] = key_at(p);
+        // walk: lane L emits outputs [L*R, L*R + R) of this unit
+        const uint32_t i0 = lane * R;
+        U out[R];
+        if (i0 < imax) {
+          // select the (h+1)-th live position of row_L
+          uint32_t cnt = 0, cw = 0, cb = 0;
+          for (;; ++cw) {
+            cb = rows[row_addr(lane, cw)];
+            const uint32_t pc = __popc(cb);
+            if (cnt + pc > h) break;
+            cnt += pc;
+          }
+          uint32_t p = cw * 32 + __fns(cb, 0, (int)(h - cnt) + 1);
+          out[0] = key_at(p);
 #pragma unroll
-        for (int t = 1; t < R; ++t) {
-          if (i0 + t < imax) {
-            const uint32_t ab = rab[(t - 1) * 32 + lane];
-            const uint32_t a = ab & 0xFFFF, b = ab >> 16;
-            // Delete(A, i-1) and Undelete(B, i-1): clear / set one live bit each; the
-            // cached cursor word is authoritative for word cw, shared memory for the rest
-            if ((a >> 5) == cw) cb &= ~(1u << (a & 31)); else rows[row_addr(lane, a >> 5)] &= ~(1u << (a & 31));
-            if ((b >> 5) == cw) cb |= 1u << (b & 31); else rows[row_addr(lane, b >> 5)] |= 1u << (b & 31);
-            const bool up = (a == p) ? (b > p) : (a < p && b > p);
-            const bool down = (a == p) ? (b < p) : (a > p && b < p);
-            if (up) {
-              const uint32_t sh = (p & 31) + 1;
-              uint32_t m = sh < 32 ? cb & (0xFFFFFFFFu << sh) : 0u;
-              while (m == 0) { rows[row_addr(lane, cw)] = cb; ++cw; cb = rows[row_addr(lane, cw)]; m = cb; }
-              p = cw * 32 + __ffs(m) - 1;
-            } else if (down) {
-              uint32_t m = cb & ((1u << (p & 31)) - 1u);
-              while (m == 0) { rows[row_addr(lane, cw)] = cb; --cw; cb = rows[row_addr(lane, cw)]; m = cb; }
-              p = cw * 32 + 31 - __clz(m);
+          for (int t = 1; t < R; ++t) {
+            if (i0 + t < imax) {
+              const uint32_t ab = rab[(t - 1) * 32 + lane];
+              const uint32_t a = ab & 0xFFFF, b = ab >> 16;
+              // Delete(A, i-1) and Undelete(B, i-1): clear / set one live bit each; the
+              // cached cursor word is authoritative for word cw, shared memory for the rest
+              if ((a >> 5) == cw) cb &= ~(1u << (a & 31)); else rows[row_addr(lane, a >> 5)] &= ~(1u << (a & 31));
+              if ((b >> 5) == cw) cb |= 1u << (b & 31); else rows[row_addr(lane, b >> 5)] |= 1u << (b & 31);
+              const bool up = (a == p) ? (b > p) : (a < p && b > p);
+              const bool down = (a == p) ? (b < p) : (a > p && b < p);
+              if (up) {
+                const uint32_t sh = (p & 31) + 1;
+                uint32_t m = sh < 32 ? cb & (0xFFFFFFFFu << sh) : 0u;
+                while (m == 0) { rows[row_addr(lane, cw)] = cb; ++cw; cb = rows[row_addr(lane, cw)]; m = cb; }
+                p = cw * 32 + __ffs(m) - 1;
+              } else if (down) {
+                uint32_t m = cb & ((1u << (p & 31)) - 1u);
+                while (m == 0) { rows[row_addr(lane, cw)] = cb; --cw; cb = rows[row_addr(lane, cw)]; m = cb; }
+                p = cw * 32 + 31 - __clz(m);
+              }
+              out[t] = key_at(p);
             }
-            out[t] = key_at(p);
           }
         }
-      }
-      __syncwarp();  // rows are dead: reuse them as the output staging area
+        __syncwarp();  // rows are dead: reuse them as the output staging area
 #pragma unroll
-      for (int t = 0; t < R; ++t)
-        if (i0 + t < imax) ost[i0 + t + ((i0 + t) >> 5)] = out[t];
-      __syncwarp();
-      TV* yo = y + u * k;
-      for (uint32_t i = lane; i < imax; i += 32) yo[i] = Tr::dec(ost[i + (i >> 5)]);
+        for (int t = 0; t < R; ++t)
+          if (i0 + t < imax) ost[i0 + t + ((i0 + t) >> 5)] = out[t];
+        __syncwarp();
+        TV* yo = y + u * k;
+        for (uint32_t i = lane; i < imax; i += 32) yo[i] = Tr::dec(ost[i + (i >> 5)]);
+      }
     }
     prev_row = row;
     prev_tile = tr;
