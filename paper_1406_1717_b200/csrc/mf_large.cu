@@ -66,13 +66,16 @@ template <int DT>
 struct Layout {
   using U = typename Traits<DT>::U;
   using E = Elem<U>;
-  size_t off_s0, off_s1, off_mk, off_org, off_rab, off_live, total;
+  size_t off_s0, off_s1, off_split, off_mk, off_org, off_rab, off_live, total;
   Layout(const LargeGeom& L, bool sort_only) {
     const uint64_t nel = (uint64_t)L.g.rows * L.nb * L.g.k;
     const uint64_t nu = (uint64_t)L.g.rows * L.g.units;
     size_t o = 0;
     off_s0 = o; o = align_up(o + sizeof(E) * nel, 256);
     off_s1 = o; o = align_up(o + sizeof(E) * nel, 256);
+    const uint64_t ntiles = std::max<uint64_t>((uint64_t)L.g.rows * L.nb * L.mtiles,
+                                               (uint64_t)L.g.rows * L.g.units * L.tiles2);
+    off_split = o; o = align_up(o + sizeof(uint2) * ntiles, 256);
     off_mk = off_org = off_rab = off_live = o;
     if (!sort_only) {
       off_mk = o; o = align_up(o + sizeof(U) * nu * L.nqp, 256);
@@ -96,10 +99,14 @@ cudaError_t sort_blocks(const LargeGeom& L, unsigned char* ws, const Layout<DT>&
   ml_tile_sort<DT><<<dim3((unsigned)(L.nb * L.tiles), L.g.rows), LNT, TileSort<U>::smem, s>>>(L, bufs[0]);
   ++*launches;
   int cur = 0;
+  uint2* splits = reinterpret_cast<uint2*>(ws + lay.off_split);
+  const uint64_t ptiles = (uint64_t)L.g.rows * L.nb * L.mtiles;
   for (uint64_t run = L.TS; run < L.g.k; run *= 2) {
+    ml_partition_pass<DT><<<(unsigned)((ptiles + 127) / 128), 128, 0, s>>>(L, bufs[cur], splits, (uint32_t)run,
+                                                                         ptiles);
     ml_merge_pass<DT><<<dim3((unsigned)(L.nb * L.mtiles), L.g.rows), LNT, merge_tile_smem<U>(), s>>>(
-        L, bufs[cur], bufs[cur ^ 1], (uint32_t)run);
-    ++*launches;
+        L, bufs[cur], bufs[cur ^ 1], (uint32_t)run, splits);
+    *launches += 2;
     cur ^= 1;
   }
   *result = bufs[cur];
@@ -122,8 +129,12 @@ cudaError_t run_large_dt(const Geom& g, void* wsv, size_t ws_bytes, cudaStream_t
   uint32_t* live = reinterpret_cast<uint32_t*>(ws + lay.off_live);
   const uint64_t nu = (uint64_t)g.rows * g.units;
   const size_t um = merge_tile_smem<U>() + sizeof(uint32_t) * 8 * L.C;
-  ml_unit_merge<DT><<<dim3((unsigned)(g.units * L.tiles2), g.rows), LNT, um, s>>>(L, sorted, mk, org, rab, live);
-  ++*launches;
+  uint2* splits = reinterpret_cast<uint2*>(ws + lay.off_split);
+  const uint64_t utiles = (uint64_t)g.rows * g.units * L.tiles2;
+  ml_partition_units<DT><<<(unsigned)((utiles + 127) / 128), 128, 0, s>>>(L, sorted, splits, utiles);
+  ml_unit_merge<DT><<<dim3((unsigned)(g.units * L.tiles2), g.rows), LNT, um, s>>>(L, sorted, mk, org, rab, live,
+                                                                                  splits);
+  *launches += 2;
   const uint64_t nchunks = nu * L.C;
   ml_walk<DT><<<(unsigned)((nchunks + LNT - 1) / LNT), LNT, sizeof(U) * 32 * 9 * (LNT / 32), s>>>(
       L, mk, org, rab, live, nchunks);

@@ -115,16 +115,9 @@ __device__ __forceinline__ uint32_t warp_split(const E* X, uint32_t lx, const E*
 // through padded smem; thread `tid` merges outputs [tid*LR2, tid*LR2 + LR2) into v and
 // returns how many it produced; `srcB[r]` tells which side each came from.
 template <typename E, typename Before>
-__device__ __forceinline__ int merge_tile(E* s, const E* X, uint32_t lx, const E* Y, uint32_t ly, uint32_t d0,
-                                          uint32_t d1, Before before, E (&v)[LR2], bool (&srcB)[LR2],
-                                          uint32_t* split, uint32_t& nx_out) {
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp < 2) {
-    const uint32_t a = warp_split(X, lx, Y, ly, warp ? d1 : d0, before, lane);
-    if (lane == 0) split[warp] = a;
-  }
-  __syncthreads();
-  const uint32_t a0 = split[0], a1 = split[1];
+__device__ __forceinline__ int merge_tile(E* s, const E* X, const E* Y, uint32_t d0, uint32_t d1, uint2 sp,
+                                          Before before, E (&v)[LR2], bool (&srcB)[LR2], uint32_t& nx_out) {
+  const uint32_t a0 = sp.x, a1 = sp.y;   // merge-path splits, precomputed by ml_partition_*
   const uint32_t b0 = d0 - a0, b1 = d1 - a1;
   const uint32_t nx = a1 - a0, ny = b1 - b0;
   for (uint32_t i = threadIdx.x; i < nx + ny; i += LNT) s[pad<LPS>(i)] = i < nx ? X[a0 + i] : Y[b0 + i - nx];
@@ -159,15 +152,67 @@ __device__ __forceinline__ int merge_tile(E* s, const E* X, uint32_t lx, const E
   return cnt;
 }
 
+// merge-path split of diagonal d over X[0,lx) and Y[0,ly) under `before(x, y)`
+template <typename E, typename Before>
+__device__ __forceinline__ uint32_t merge_split(const E* X, uint32_t lx, const E* Y, uint32_t ly, uint32_t d,
+                                                Before before) {
+  uint32_t lo = d > ly ? d - ly : 0, hi = d < lx ? d : lx;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (before(X[mid], Y[d - 1 - mid])) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// ---- merge-path partitions: the (start, end) split of every merge tile, computed up front
+// by one thread per tile so the merge kernels start streaming immediately ---------------
+template <int DT>
+__global__ void ml_partition_pass(LargeGeom L, const Elem<typename Traits<DT>::U>* in, uint2* splits, uint32_t run,
+                                  uint64_t total) {
+  using E = Elem<typename Traits<DT>::U>;
+  const uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= total) return;
+  const uint32_t t = id % L.mtiles;
+  const uint64_t rb = id / L.mtiles;                 // row * nb + b
+  const uint32_t k = L.g.k;
+  const uint32_t p0 = t * LQ;
+  const uint32_t x0 = p0 / (2 * run) * (2 * run);
+  const uint32_t lx = min(run, k - x0);
+  const uint32_t y0 = x0 + lx;
+  const uint32_t ly = y0 < k ? min(run, k - y0) : 0;
+  const uint32_t d0 = p0 - x0, d1 = min(d0 + LQ, lx + ly);
+  const E* X = in + rb * k + x0;
+  const E* Y = in + rb * k + y0;
+  auto before = [](const E& a, const E& c) { return E::less(a, c); };
+  splits[id] = make_uint2(merge_split(X, lx, Y, ly, d0, before), merge_split(X, lx, Y, ly, d1, before));
+}
+
+template <int DT>
+__global__ void ml_partition_units(LargeGeom L, const Elem<typename Traits<DT>::U>* S, uint2* splits,
+                                   uint64_t total) {
+  using E = Elem<typename Traits<DT>::U>;
+  const uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= total) return;
+  const uint32_t t = id % L.tiles2;
+  const uint64_t ug = id / L.tiles2;                 // row * units + u
+  const uint64_t row = ug / L.g.units, u = ug % L.g.units;
+  const uint32_t k = L.g.k;
+  const E* A = S + (row * L.nb + u) * k;
+  const E* B = A + k;
+  const uint32_t d0 = t * LQ, d1 = min(d0 + LQ, L.nq);
+  auto before = [](const E& a, const E& c) { return a.key() <= c.key(); };
+  splits[id] = make_uint2(merge_split(A, k, B, k, d0, before), merge_split(A, k, B, k, d1, before));
+}
+
 // ---- phase 1b: one global merge pass (runs of length `run` within every block) --------
 template <int DT>
 __global__ void __launch_bounds__(LNT) ml_merge_pass(LargeGeom L, const Elem<typename Traits<DT>::U>* in,
-                                                     Elem<typename Traits<DT>::U>* out, uint32_t run) {
+                                                     Elem<typename Traits<DT>::U>* out, uint32_t run,
+                                                     const uint2* splits) {
   using U = typename Traits<DT>::U;
   using E = Elem<U>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   E* s = reinterpret_cast<E*>(smem_raw);
-  __shared__ uint32_t split[2];
   const uint64_t row = blockIdx.y;
   const uint64_t b = blockIdx.x / L.mtiles;
   const uint32_t t = blockIdx.x % L.mtiles;
@@ -184,7 +229,8 @@ __global__ void __launch_bounds__(LNT) ml_merge_pass(LargeGeom L, const Elem<typ
   E v[LR2];
   bool srcB[LR2];
   uint32_t nx;
-  const int cnt = merge_tile(s, in + base + x0, lx, in + base + y0, ly, d0, d1, before, v, srcB, split, nx);
+  const uint2 sp = splits[(row * L.nb + b) * L.mtiles + t];
+  const int cnt = merge_tile(s, in + base + x0, in + base + y0, d0, d1, sp, before, v, srcB, nx);
   __syncthreads();
   const int dd = threadIdx.x * LR2;
 #pragma unroll
@@ -199,13 +245,12 @@ __global__ void __launch_bounds__(LNT) ml_merge_pass(LargeGeom L, const Elem<typ
 template <int DT>
 __global__ void __launch_bounds__(LNT, 4) ml_unit_merge(LargeGeom L, const Elem<typename Traits<DT>::U>* S,
                                                      typename Traits<DT>::U* mk, uint32_t* org, uint2* rab,
-                                                     uint32_t* live) {
+                                                     uint32_t* live, const uint2* splits) {
   using U = typename Traits<DT>::U;
   using E = Elem<U>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   E* s = reinterpret_cast<E*>(smem_raw);                                     // merge tile
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw + sizeof(E) * (LQ + (LQ >> LPS) + 1));  // [4][2][C]
-  __shared__ uint32_t split[2];
   const uint64_t row = blockIdx.y;
   const uint64_t u = blockIdx.x / L.tiles2;
   const uint32_t t = blockIdx.x % L.tiles2;
@@ -220,7 +265,8 @@ __global__ void __launch_bounds__(LNT, 4) ml_unit_merge(LargeGeom L, const Elem<
   E v[LR2];
   bool srcB[LR2];
   uint32_t nx;
-  const int cnt = merge_tile(s, A, k, B, k, d0, d1, before, v, srcB, split, nx);
+  const uint2 sp = splits[(row * L.g.units + u) * L.tiles2 + t];
+  const int cnt = merge_tile(s, A, B, d0, d1, sp, before, v, srcB, nx);
   const int dd = threadIdx.x * LR2;
   uint2* ro = rab + ug * (uint64_t)L.C * L.CL;
   __syncthreads();
