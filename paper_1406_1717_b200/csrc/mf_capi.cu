@@ -66,7 +66,7 @@ mf_status run_rows(mf_context* ctx, mf_dtype dtype, const void* d_x, size_t rows
   if (!dtype_ok(dtype)) return MF_BAD_ARG;
   ctx->launches = 0;
   if (keep == 0 || rows == 0) return MF_OK;
-  if (!d_x || !d_y || ld_x < n || ld_y < keep || rows > 65535) return MF_BAD_ARG;
+  if (!d_x || !d_y || ld_x < n || ld_y < keep || rows > 0xFFFFFFFFull) return MF_BAD_ARG;
   if (cudaSetDevice(ctx->device) != cudaSuccess) return MF_NO_DEVICE;
   mf::Geom g{};
   g.x = d_x; g.y = d_y; g.n = n; g.ld_x = ld_x; g.ld_y = ld_y;
@@ -81,10 +81,19 @@ mf_status run_rows(mf_context* ctx, mf_dtype dtype, const void* d_x, size_t rows
   } else if (cls == MF_CLASS_MEDIUM) {
     e = mf::launch_medium(dtype, g, s, &ctx->launches);
   } else {
-    const size_t need = mf::large_workspace_bytes(dtype, g);
-    st = grow(&ctx->ws, &ctx->ws_bytes, need);
-    if (st != MF_OK) return st;
-    e = mf::run_large(dtype, g, ctx->ws, ctx->ws_bytes, s, &ctx->launches);
+    // the large-k kernels put rows on grid.y (<= 65535): run row groups
+    const size_t w = dtype_size(dtype);
+    e = cudaSuccess;
+    for (size_t r0 = 0; r0 < rows && e == cudaSuccess; r0 += 65535) {
+      mf::Geom gg = g;
+      gg.rows = (uint32_t)std::min<size_t>(65535, rows - r0);
+      gg.x = static_cast<const char*>(d_x) + r0 * ld_x * w;
+      gg.y = static_cast<char*>(d_y) + r0 * ld_y * w;
+      const size_t need = mf::large_workspace_bytes(dtype, gg);
+      st = grow(&ctx->ws, &ctx->ws_bytes, need);
+      if (st != MF_OK) return st;
+      e = mf::run_large(dtype, gg, ctx->ws, ctx->ws_bytes, s, &ctx->launches);
+    }
   }
   return from_cuda(e);
 }
@@ -233,7 +242,7 @@ mf_status mf_median_filter_rows(mf_context* ctx, mf_dtype dtype, const void* x, 
   const size_t w = dtype_size(dtype);
   // chunk geometry: single signals by output ranges, batches by row groups
   const bool by_rows = rows > 1;
-  const size_t rows_per = by_rows ? std::max<size_t>(1, kChunkElems / n) : 1;
+  const size_t rows_per = by_rows ? std::max<size_t>(1, kChunkElems / n) : 1;  // rows per chunk
   const size_t out_per = by_rows ? keep : std::min(keep, std::max<size_t>(kChunkElems, 16 * k));
   const size_t nchunks = by_rows ? (rows + rows_per - 1) / rows_per : (keep + out_per - 1) / out_per;
   const size_t in_slot = ((by_rows ? rows_per * n : out_per + k - 1) * w + 255) / 256 * 256;
