@@ -13,6 +13,7 @@
 #include <concepts>
 #include <cstddef>
 #include <cstdint>
+#include <limits>
 #include <memory>
 #include <span>
 #include <stdexcept>
@@ -82,6 +83,30 @@ inline std::vector<float> median_filter(std::span<const float> x, std::size_t k)
 }
 inline std::vector<double> median_filter(std::span<const double> x, std::size_t k) {
   return detail::run<double>(x, k);
+}
+
+/// sort_via_median_filter (filter.hpp:177-205) with the filter on the GPU: each block of
+/// h+1 samples is surrounded by h copies of the type's minimum and h of its maximum, one
+/// median filter with k = 2h+1 runs over the whole gadget, and each block's sorted image
+/// is read out of the output.
+template <std::signed_integral T>
+std::vector<std::vector<T>> sort_via_median_filter(std::span<const std::vector<T>> blocks, std::size_t h) {
+  for (const auto& block : blocks)
+    if (block.size() != h + 1) throw std::invalid_argument("each block must hold h+1 samples");
+  if (blocks.empty()) return {};
+  const std::size_t k = 2 * h + 1, unit = 3 * h + 1;
+  std::vector<T> gadget;
+  gadget.reserve(blocks.size() * unit);
+  for (const auto& block : blocks) {
+    gadget.insert(gadget.end(), h, std::numeric_limits<T>::min());
+    gadget.insert(gadget.end(), block.begin(), block.end());
+    gadget.insert(gadget.end(), h, std::numeric_limits<T>::max());
+  }
+  const std::vector<T> med = median_filter<T>(std::span<const T>(gadget), k);
+  std::vector<std::vector<T>> sorted(blocks.size());
+  for (std::size_t j = 0; j < blocks.size(); ++j)
+    sorted[j].assign(med.begin() + j * unit, med.begin() + j * unit + h + 1);
+  return sorted;
 }
 
 }  // namespace medfilt::gpu

@@ -238,3 +238,45 @@ def generate_trend_f64(seed: int, n: int) -> np.ndarray:
     out = np.empty(n, dtype=np.float64)
     N.lib().mf_generate_trend_f64_host(seed, n, out.ctypes.data)
     return out
+
+
+# ---------------------------------------------------------------------------------------
+# §2 lower-bound gadget: sorting through one median-filter call
+# ---------------------------------------------------------------------------------------
+def _extremes(dtype):
+    dt = np.dtype(dtype)
+    if dt.kind == "i":
+        info = np.iinfo(dt)
+        return dt.type(info.min), dt.type(info.max)
+    ui = np.uint32 if dt.itemsize == 4 else np.uint64
+    # the two ends of IEEE totalOrder: -NaN and +NaN with all-ones payloads
+    lo = np.array([~ui(0)], dtype=ui).view(dt)[0]
+    hi = np.array([~ui(0) >> ui(1)], dtype=ui).view(dt)[0]
+    return lo, hi
+
+
+def sort_via_median_filter(blocks, h: int | None = None, *, ctx: Context | None = None) -> np.ndarray:
+    """sort_via_median_filter (filter.hpp:177-205) on the GPU: every row of `blocks`
+    (nb x (h+1)) is surrounded by h below-everything and h above-everything samples, the
+    whole gadget is median-filtered with k = 2h+1 in one call, and each block's sorted image
+    is read out of the output.  Executable form of the paper's sorting lower bound (§2)."""
+    blocks = np.asarray(blocks)
+    if blocks.ndim != 2:
+        raise ValueError("blocks must be a 2-D array (nb x (h+1))")
+    nb, h1 = blocks.shape
+    if h is None:
+        h = h1 - 1
+    if h1 != h + 1:
+        raise InvalidArgument("each block must hold h+1 samples")   # filter.hpp:179-181
+    if nb == 0:
+        return blocks.copy()
+    lo, hi = _extremes(blocks.dtype)
+    unit = 3 * h + 1
+    gadget = np.empty((nb, unit), dtype=blocks.dtype)
+    gadget[:, :h] = lo
+    gadget[:, h:2 * h + 1] = blocks
+    gadget[:, 2 * h + 1:] = hi
+    med = median_filter(gadget.ravel(), 2 * h + 1, ctx=ctx)
+    # the reference keeps medians[j*unit .. j*unit + h], filter.hpp:199-203
+    med = np.concatenate([med, np.empty(unit * nb - med.size, dtype=med.dtype)])
+    return med.reshape(nb, unit)[:, :h + 1].copy()

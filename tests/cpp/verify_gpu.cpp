@@ -93,6 +93,19 @@ int main(int argc, char** argv) {
       if (std::string(e.what()) != expect[i]) ++failures;
     }
   }
+  // the §2 reduction witness through the GPU filter (filter.hpp:177-205)
+  {
+    const std::vector<std::vector<std::int64_t>> blocks = {{3, 1}, {9, 7}};
+    const auto got = medfilt::gpu::sort_via_median_filter<std::int64_t>(blocks, 1);
+    const auto want = medfilt::sort_via_median_filter<std::int64_t>(blocks, 1);
+    if (got != want) ++failures;
+    medfilt::SplitMix64 g(99);
+    std::vector<std::vector<std::int64_t>> big(50, std::vector<std::int64_t>(64));
+    for (auto& b : big) for (auto& v : b) v = static_cast<std::int64_t>(g.next());
+    if (medfilt::gpu::sort_via_median_filter<std::int64_t>(big, 63) !=
+        medfilt::sort_via_median_filter<std::int64_t>(big, 63))
+      ++failures;
+  }
   std::printf("verify_gpu: exhaustive=%zu random=%zu failures=%zu\n", exhaustive, random, failures);
   return failures == 0 ? 0 : 1;
 }
