@@ -10,13 +10,13 @@ namespace {
 // smaller R has a smaller footprint and gets more warps.
 template <int DT, int R> struct WarpsFor {
   static constexpr bool wide = sizeof(typename Traits<DT>::U) == 8;
-  static constexpr int value = R >= 32 ? (wide ? 2 : 4) : (R >= 16 ? 4 : 8);
+  static constexpr int value = R >= 32 ? 2 : (R >= 16 ? 4 : 8);
 };
 
 template <int DT, int R>
 cudaError_t launch_r(const Geom& g, cudaStream_t s) {
   constexpr int W = WarpsFor<DT, R>::value;
-  constexpr int WP = 1;  // warps per block pair (team); 2 measured slower at k=1023 (register-bound)
+  constexpr int WP = R >= 32 ? 2 : 1;  // warps per block pair (team); k <= 511 measured faster with 1
   using C = MediumCfg<DT, R, W, WP>;
   auto kern = mf_medium_kernel<DT, R, W, WP>;
   static int resident = 0;  // CTAs per SM (per process; the attribute is idempotent)

@@ -42,13 +42,15 @@ struct MediumCfg {
   static constexpr int BS = 32 * R;        // block slot capacity (>= k)
   static constexpr int NW = 2 * R;         // words per merged row (2k bits <= 64R)
   static constexpr int RS = R / WP;        // elements per lane in the team block sort
+  static constexpr int CH = 32 * WP;       // walk chunks per pair (one per team lane)
+  static constexpr int SR = R / WP;        // steps per chunk
   // padded element index: blocked per-lane writes hit distinct banks (8-byte elements)
   static constexpr int PS = pad_shift<RS>();
   static constexpr int SLOT = BS + (BS >> PS) + 1;
   static constexpr size_t sz_sorted = sizeof(E) * SLOT * (W + 1);
   static constexpr size_t sz_src = sizeof(uint16_t) * 2 * BS;  // merged pos -> (isB, sorted pos)
   static constexpr size_t sz_rab = sizeof(uint32_t) * BS;      // RA | RB << 16, transposed [t][lane]
-  static constexpr size_t sz_rows_bits = sizeof(uint32_t) * NW * 32;
+  static constexpr size_t sz_rows_bits = sizeof(uint32_t) * NW * CH;
   static constexpr size_t sz_stage = sizeof(U) * (BS + BS / 32 + 1);
   // the rows area doubles as the output staging area after the walk
   static constexpr size_t sz_rows = (sz_rows_bits > sz_stage ? sz_rows_bits : sz_stage + 15) / 16 * 16;
@@ -59,7 +61,8 @@ struct MediumCfg {
 
 // rows[L][w] lives at w*32 + (L ^ (w & 31)): the prefix pass (lane = word, loop
 // over L) and the walk (lane = L, data-dependent word) are both bank-spread.
-__device__ __forceinline__ uint32_t row_addr(uint32_t L, uint32_t w) { return w * 32 + (L ^ (w & 31)); }
+template <int CH>
+__device__ __forceinline__ uint32_t row_addr(uint32_t L, uint32_t w) { return w * CH + (L ^ (w & (CH - 1))); }
 
 // A "team" of WP warps owns one block pair: it sorts the pair's B block together (WP warp
 // sorts + a team merge level), runs the pair merge and the XOR prefix with 32*WP lanes,
@@ -72,7 +75,7 @@ __global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t
   using U = typename C::U;
   using E = typename C::E;
   using TV = typename Tr::T;
-  constexpr int NW = C::NW, PS = C::PS, SLOT = C::SLOT, RS = C::RS;
+  constexpr int NW = C::NW, PS = C::PS, SLOT = C::SLOT, RS = C::RS, CH = C::CH, SR = C::SR;
   constexpr int TL = 32 * WP;        // team lanes
   extern __shared__ __align__(16) unsigned char smem[];
   E* ring = reinterpret_cast<E*>(smem);
@@ -132,7 +135,7 @@ __global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t
       const E* A = slot(team);
       const E* B = slot(team + 1);
 
-      for (uint32_t i = tl; i < NW * 32; i += TL) rows[i] = 0;
+      for (uint32_t i = tl; i < NW * CH; i += TL) rows[i] = 0;
       for (uint32_t w = tl; w < NW; w += TL) abits[w] = 0;
       team_sync();
 
@@ -157,11 +160,11 @@ __global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t
           const bool valid = q < (int)nq;
           const bool takeA = (ib >= K) || (ia < K && ea.key() <= eb.key());
           const uint32_t idx = sel(takeA, ea.idx(), eb.idx());
-          const uint32_t c = idx / R;            // owning lane (chunk) of this element
+          const uint32_t c = idx / SR;           // owning team lane (chunk) of this element
           if (valid) {
-            atomicOr(&rows[row_addr(c, q >> 5)], 1u << (q & 31));
+            atomicOr(&rows[row_addr<CH>(c, q >> 5)], 1u << (q & 31));
             src[q] = (uint16_t)sel(takeA, (uint32_t)ia, 0x8000u | (uint32_t)ib);
-            rab16[2 * ((idx % R) * 32 + c) + (takeA ? 0 : 1)] = (uint16_t)q;
+            rab16[2 * ((idx % SR) * CH + c) + (takeA ? 0 : 1)] = (uint16_t)q;
           }
           amask |= (uint64_t)(valid && takeA) << r;
           ia += takeA;
@@ -189,8 +192,8 @@ __global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t
       for (uint32_t w = tl; w < nw; w += TL) {
         uint32_t acc = abits[w];
 #pragma unroll 8
-        for (uint32_t L = 0; L < 32; ++L) {
-          const uint32_t a = row_addr(L, w);
+        for (uint32_t L = 0; L < (uint32_t)CH; ++L) {
+          const uint32_t a = row_addr<CH>(L, w);
           const uint32_t dlt = rows[a];
           rows[a] = acc;
           acc ^= dlt;
@@ -198,20 +201,20 @@ __global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t
       }
       team_sync();
 
-      if (sub == 0) {
+      {
         auto key_at = [&](uint32_t p) -> U {
           const uint32_t s = src[p];
           return (s & 0x8000u) ? B[pad<PS>(s & 0x7FFF)].key() : A[pad<PS>(s)].key();
         };
 
-        // walk: lane L emits outputs [L*R, L*R + R) of this unit
-        const uint32_t i0 = lane * R;
-        U out[R];
+        // walk: team lane L emits outputs [L*SR, L*SR + SR) of this unit
+        const uint32_t i0 = tl * SR;
+        U out[SR];
         if (i0 < imax) {
           // select the (h+1)-th live position of row_L
           uint32_t cnt = 0, cw = 0, cb = 0;
           for (;; ++cw) {
-            cb = rows[row_addr(lane, cw)];
+            cb = rows[row_addr<CH>(tl, cw)];
             const uint32_t pc = __popc(cb);
             if (cnt + pc > h) break;
             cnt += pc;
@@ -219,37 +222,37 @@ __global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t
           uint32_t p = cw * 32 + __fns(cb, 0, (int)(h - cnt) + 1);
           out[0] = key_at(p);
 #pragma unroll
-          for (int t = 1; t < R; ++t) {
+          for (int t = 1; t < SR; ++t) {
             if (i0 + t < imax) {
-              const uint32_t ab = rab[(t - 1) * 32 + lane];
+              const uint32_t ab = rab[(t - 1) * CH + tl];
               const uint32_t a = ab & 0xFFFF, b = ab >> 16;
               // Delete(A, i-1) and Undelete(B, i-1): clear / set one live bit each; the
               // cached cursor word is authoritative for word cw, shared memory for the rest
-              if ((a >> 5) == cw) cb &= ~(1u << (a & 31)); else rows[row_addr(lane, a >> 5)] &= ~(1u << (a & 31));
-              if ((b >> 5) == cw) cb |= 1u << (b & 31); else rows[row_addr(lane, b >> 5)] |= 1u << (b & 31);
+              if ((a >> 5) == cw) cb &= ~(1u << (a & 31)); else rows[row_addr<CH>(tl, a >> 5)] &= ~(1u << (a & 31));
+              if ((b >> 5) == cw) cb |= 1u << (b & 31); else rows[row_addr<CH>(tl, b >> 5)] |= 1u << (b & 31);
               const bool up = (a == p) ? (b > p) : (a < p && b > p);
               const bool down = (a == p) ? (b < p) : (a > p && b < p);
               if (up) {
                 const uint32_t sh = (p & 31) + 1;
                 uint32_t m = sh < 32 ? cb & (0xFFFFFFFFu << sh) : 0u;
-                while (m == 0) { rows[row_addr(lane, cw)] = cb; ++cw; cb = rows[row_addr(lane, cw)]; m = cb; }
+                while (m == 0) { rows[row_addr<CH>(tl, cw)] = cb; ++cw; cb = rows[row_addr<CH>(tl, cw)]; m = cb; }
                 p = cw * 32 + __ffs(m) - 1;
               } else if (down) {
                 uint32_t m = cb & ((1u << (p & 31)) - 1u);
-                while (m == 0) { rows[row_addr(lane, cw)] = cb; --cw; cb = rows[row_addr(lane, cw)]; m = cb; }
+                while (m == 0) { rows[row_addr<CH>(tl, cw)] = cb; --cw; cb = rows[row_addr<CH>(tl, cw)]; m = cb; }
                 p = cw * 32 + 31 - __clz(m);
               }
               out[t] = key_at(p);
             }
           }
         }
-        __syncwarp();  // rows are dead: reuse them as the output staging area
+        team_sync();  // rows are dead: reuse them as the output staging area
 #pragma unroll
-        for (int t = 0; t < R; ++t)
+        for (int t = 0; t < SR; ++t)
           if (i0 + t < imax) ost[i0 + t + ((i0 + t) >> 5)] = out[t];
-        __syncwarp();
+        team_sync();
         TV* yo = y + u * k;
-        for (uint32_t i = lane; i < imax; i += 32) yo[i] = Tr::dec(ost[i + (i >> 5)]);
+        for (uint32_t i = tl; i < imax; i += TL) yo[i] = Tr::dec(ost[i + (i >> 5)]);
       }
     }
     prev_row = row;
