@@ -76,13 +76,57 @@ __device__ __forceinline__ void merge_levels(E* s, int b0, int tid, int run0, in
 
 // Warp sort of 32*R register-loaded elements (v, any distribution over lanes) into
 // s[b0 .. b0 + 32R) (padded layout, sorted ascending).
+// Bitonic merge levels in registers: after it, every group of G = 2^levels lanes holds one
+// sorted run of G*R elements (lane offset o of the group holds elements [o*R, o*R + R)).
+// Each level is a mirror stage (element i against element G*R-1-i of the partner lane
+// o ^ (G-1)), then half-cleaners: across lanes for distances >= R (partner o ^ (d/R)) and
+// inside the lane below that.  No shared memory, no searches; the elements are totally
+// ordered, so the result equals any other sort's.
+template <typename E, int R, int LEVELS>
+__device__ __forceinline__ void warp_bitonic_levels(E (&v)[R], uint32_t lane) {
+#pragma unroll
+  for (int m = 1; m <= LEVELS; ++m) {
+    const int G = 1 << m;
+    {  // mirror stage
+      const bool lower = (lane & (G >> 1)) == 0;
+      E t[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) t[r] = shfl_xor(v[R - 1 - r], G - 1);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const bool lt = E::less(v[r], t[r]);
+        v[r] = E::select(lt == lower, v[r], t[r]);
+      }
+    }
+#pragma unroll
+    for (int dl = G >> 2; dl >= 1; dl >>= 1) {  // cross-lane half-cleaners, lane distance dl
+      const bool lower = (lane & dl) == 0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const E p = shfl_xor(v[r], dl);
+        const bool lt = E::less(v[r], p);
+        v[r] = E::select(lt == lower, v[r], p);
+      }
+    }
+#pragma unroll
+    for (int d = R >> 1; d >= 1; d >>= 1) {      // in-lane half-cleaners
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if ((r & d) == 0) E::cswap(v[r], v[r + d]);
+    }
+  }
+}
+
 template <typename E, int R, int PS>
 __device__ __forceinline__ void warp_sort_regs(E (&v)[R], E* s, int b0, uint32_t lane) {
+  // register bitonic levels before the smem merges (measured: 64-bit keys gain nothing)
+  constexpr int BL = sizeof(E) > 8 ? 0 : (R >= 16 ? 2 : 4);
   sort_regs<R>(v);
+  warp_bitonic_levels<E, R, BL>(v, lane);
 #pragma unroll
   for (int r = 0; r < R; ++r) s[pad<PS>(b0 + lane * R + r)] = v[r];
   __syncwarp();
-  merge_levels<E, R, PS, false>(s, b0, lane, R, 32 * R, v);
+  merge_levels<E, R, PS, false>(s, b0, lane, R << BL, 32 * R, v);
 }
 
 // Raw (un-keyed) coalesced load of block `blk` of a row: element e = lane + 32r.  Slots

@@ -88,6 +88,13 @@ template <> struct Elem<uint64_t> {
   }
 };
 
+__device__ __forceinline__ Elem<uint32_t> shfl_xor(const Elem<uint32_t>& e, int m) {
+  Elem<uint32_t> r; r.v = __shfl_xor_sync(0xFFFFFFFFu, e.v, m); return r;
+}
+__device__ __forceinline__ Elem<uint64_t> shfl_xor(const Elem<uint64_t>& e, int m) {
+  Elem<uint64_t> r; r.k = __shfl_xor_sync(0xFFFFFFFFu, e.k, m); r.i = __shfl_xor_sync(0xFFFFFFFFu, e.i, m); return r;
+}
+
 template <int K, int I, typename E>
 __device__ __forceinline__ void net_apply(E* v) {
   if constexpr (I < OEM<K>::net.n) {
