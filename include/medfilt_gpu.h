@@ -46,7 +46,8 @@ typedef enum { MF_I32 = 0, MF_I64 = 1, MF_F32 = 2, MF_F64 = 3 } mf_dtype;
 typedef enum { MF_CLASS_AUTO = -1, MF_CLASS_SMALL = 0, MF_CLASS_MEDIUM = 1, MF_CLASS_LARGE = 2 } mf_class;
 
 typedef enum {
-  MF_OPT_FORCE_CLASS = 0   /* value: mf_class; a forced class must support k */
+  MF_OPT_FORCE_CLASS = 0,    /* value: mf_class; a forced class must support k */
+  MF_OPT_PIPELINE_CHUNK = 1  /* value: largest host-pipeline chunk in samples (0 = default 2^23) */
 } mf_option;
 
 typedef struct mf_context mf_context;

@@ -16,6 +16,7 @@ MF_BAD_ARG, MF_CUDA_ERROR, MF_OUT_OF_MEMORY, MF_NO_DEVICE = 5, 6, 7, 8
 MF_I32, MF_I64, MF_F32, MF_F64 = 0, 1, 2, 3
 MF_CLASS_AUTO, MF_CLASS_SMALL, MF_CLASS_MEDIUM, MF_CLASS_LARGE = -1, 0, 1, 2
 MF_OPT_FORCE_CLASS = 0
+MF_OPT_PIPELINE_CHUNK = 1
 MF_GEN_UNIFORM_F32, MF_GEN_UNIFORM_F64, MF_GEN_MOD_I32 = 0, 1, 2
 
 # Every symbol include/medfilt_gpu.h declares (checked by tests/test_abi.py).

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "../../include/medfilt_gpu.h"
 #include "mf_launch.h"
@@ -21,10 +22,11 @@ struct mf_context {
   void* io = nullptr;          // grow-only device buffers for the host entry points
   size_t io_bytes = 0;
   int force_class = MF_CLASS_AUTO;
+  size_t chunk_elems = size_t(1) << 23;  // largest host-pipeline chunk (samples)
   uint64_t launches = 0;
-  // host-entry pipeline: H2D / compute / D2H on three streams, kNumSlots chunks in flight
+  // host-entry pipeline: H2D / compute / D2H on three streams, up to 4 chunks in flight
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
-  cudaEvent_t ev_in[3] = {}, ev_done[3] = {}, ev_out[3] = {};
+  cudaEvent_t ev_in[4] = {}, ev_done[4] = {}, ev_out[4] = {};
   std::mutex mu;
 };
 
@@ -174,7 +176,7 @@ void mf_context_destroy(mf_context* ctx) {
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->s_h2d) cudaStreamSynchronize(ctx->s_h2d), cudaStreamDestroy(ctx->s_h2d);
   if (ctx->s_d2h) cudaStreamSynchronize(ctx->s_d2h), cudaStreamDestroy(ctx->s_d2h);
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < 4; ++i) {
     if (ctx->ev_in[i]) cudaEventDestroy(ctx->ev_in[i]);
     if (ctx->ev_done[i]) cudaEventDestroy(ctx->ev_done[i]);
     if (ctx->ev_out[i]) cudaEventDestroy(ctx->ev_out[i]);
@@ -187,6 +189,11 @@ mf_status mf_context_set_option(mf_context* ctx, mf_option opt, long value) {
   if (opt == MF_OPT_FORCE_CLASS) {
     if (value < MF_CLASS_AUTO || value > MF_CLASS_LARGE) return MF_BAD_ARG;
     ctx->force_class = (int)value;
+    return MF_OK;
+  }
+  if (opt == MF_OPT_PIPELINE_CHUNK) {
+    if (value < 0) return MF_BAD_ARG;
+    ctx->chunk_elems = value == 0 ? size_t(1) << 23 : std::max<size_t>(1024, (size_t)value);
     return MF_OK;
   }
   return MF_BAD_ARG;
@@ -210,9 +217,31 @@ mf_status mf_median_filter_device(mf_context* ctx, mf_dtype dtype, const void* d
   return mf_median_filter_rows_device(ctx, dtype, d_x, 1, n, n, k, d_y, keep ? keep : 1, stream);
 }
 
+// Chunk sizes for the host pipeline: cmin, 2*cmin, 4*cmin, ... up to cmax at the head,
+// the mirror image at the tail, cmax-sized chunks in between.  Inputs too short for both ramps get equal chunks of about cmin.
+static std::vector<size_t> chunk_schedule(size_t total, size_t cmin, size_t cmax) {
+  std::vector<size_t> ramp;
+  size_t ramp_sum = 0;
+  for (size_t s = cmin; s < cmax; s *= 2) ramp.push_back(s), ramp_sum += s;
+  std::vector<size_t> out;
+  if (total <= 2 * ramp_sum || ramp.empty()) {
+    const size_t unit = ramp.empty() ? cmax : cmin;
+    const size_t n = std::max<size_t>(1, (total + unit - 1) / unit);
+    for (size_t i = 0; i < n; ++i) out.push_back(total / n + (i < total % n ? 1 : 0));
+    return out;
+  }
+  out = ramp;
+  // middle: cmax-sized chunks (DMA-friendly offsets), the remainder in the last one
+  size_t mid = total - 2 * ramp_sum;
+  for (; mid > cmax; mid -= cmax) out.push_back(cmax);
+  if (mid) out.push_back(mid);
+  out.insert(out.end(), ramp.rbegin(), ramp.rend());
+  return out;
+}
+
 // Host entry: the literal drop-in.  The signal (or batch) is cut into chunks of about
 // kChunkElems outputs -- contiguous output ranges with a (k-1)-sample input halo, or whole
-// rows -- and three chunks are kept in flight: H2D of chunk c+1, kernels of chunk c and D2H
+// rows -- and up to four chunks are kept in flight: H2D of chunk c+1, kernels of chunk c and D2H
 // of chunk c-1 overlap on three streams, so a call costs about the slower of the two PCIe
 // directions instead of their sum.  Blocking never changes an output.
 mf_status mf_median_filter_rows(mf_context* ctx, mf_dtype dtype, const void* x, size_t rows, size_t n,
@@ -227,8 +256,8 @@ mf_status mf_median_filter_rows(mf_context* ctx, mf_dtype dtype, const void* x, 
   if (keep == 0 || rows == 0) return MF_OK;
   if (!x || !y || ld_x < n || ld_y < keep) return MF_BAD_ARG;
   if (cudaSetDevice(ctx->device) != cudaSuccess) return MF_NO_DEVICE;
-  constexpr int kNumSlots = 3;
-  constexpr size_t kChunkElems = size_t(1) << 23;
+  constexpr int kNumSlots = 4;
+  const size_t kChunkElems = ctx->chunk_elems;
   if (!ctx->s_h2d) {
     if (cudaStreamCreateWithFlags(&ctx->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking) != cudaSuccess)
@@ -240,13 +269,17 @@ mf_status mf_median_filter_rows(mf_context* ctx, mf_dtype dtype, const void* x, 
         return MF_CUDA_ERROR;
   }
   const size_t w = dtype_size(dtype);
-  // chunk geometry: single signals by output ranges, batches by row groups
+  // chunk geometry: single signals by output ranges, batches by row groups.  Chunk sizes
+  // ramp up geometrically at the start and down at the end, so the H2D of the first chunk
+  // and the D2H of the last (the parts nothing overlaps) are small.
   const bool by_rows = rows > 1;
-  const size_t rows_per = by_rows ? std::max<size_t>(1, kChunkElems / n) : 1;  // rows per chunk
-  const size_t out_per = by_rows ? keep : std::min(keep, std::max<size_t>(kChunkElems, 16 * k));
-  const size_t nchunks = by_rows ? (rows + rows_per - 1) / rows_per : (keep + out_per - 1) / out_per;
-  const size_t in_slot = ((by_rows ? rows_per * n : out_per + k - 1) * w + 255) / 256 * 256;
-  const size_t out_slot = ((by_rows ? rows_per * keep : out_per) * w + 255) / 256 * 256;
+  const size_t total = by_rows ? rows : keep;                                               // units to cut
+  const size_t cmax = by_rows ? std::max<size_t>(1, kChunkElems / n) : std::min(keep, std::max<size_t>(kChunkElems, 16 * k));
+  const size_t cmin = std::max<size_t>(by_rows ? 1 : std::min(cmax, 16 * k), cmax / 16);
+  std::vector<size_t> sizes = chunk_schedule(total, cmin, cmax);
+  const size_t nchunks = sizes.size();
+  const size_t in_slot = ((by_rows ? cmax * n : cmax + k - 1) * w + 255) / 256 * 256;
+  const size_t out_slot = ((by_rows ? cmax * keep : cmax) * w + 255) / 256 * 256;
   const int slots = (int)std::min<size_t>(kNumSlots, nchunks);
   st = grow(&ctx->io, &ctx->io_bytes, slots * (in_slot + out_slot));
   if (st != MF_OK) return st;
@@ -254,6 +287,7 @@ mf_status mf_median_filter_rows(mf_context* ctx, mf_dtype dtype, const void* x, 
   const char* hx = static_cast<const char*>(x);
   char* hy = static_cast<char*>(y);
   uint64_t launches = 0;
+  size_t start = 0;
   cudaError_t e = cudaSuccess;
   for (size_t c = 0; c < nchunks && e == cudaSuccess; ++c) {
     const int sl = (int)(c % slots);
@@ -265,16 +299,17 @@ mf_status mf_median_filter_rows(mf_context* ctx, mf_dtype dtype, const void* x, 
     }
     size_t r0 = 0, nr = 1, o0 = 0, no = keep, ni = n;
     if (by_rows) {
-      r0 = c * rows_per;
-      nr = std::min(rows_per, rows - r0);
+      r0 = start;
+      nr = sizes[c];
       e = cudaMemcpy2DAsync(d_x, n * w, hx + r0 * ld_x * w, ld_x * w, n * w, nr, cudaMemcpyHostToDevice,
                             ctx->s_h2d);
     } else {
-      o0 = c * out_per;
-      no = std::min(out_per, keep - o0);
+      o0 = start;
+      no = sizes[c];
       ni = no + k - 1;
       e = cudaMemcpyAsync(d_x, hx + o0 * w, ni * w, cudaMemcpyHostToDevice, ctx->s_h2d);
     }
+    start += sizes[c];
     if (e != cudaSuccess) break;
     if ((e = cudaEventRecord(ctx->ev_in[sl], ctx->s_h2d)) != cudaSuccess) break;
     if ((e = cudaStreamWaitEvent(ctx->stream, ctx->ev_in[sl], 0)) != cudaSuccess) break;

@@ -211,13 +211,30 @@ __global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t
         const uint32_t i0 = tl * SR;
         U out[SR];
         if (i0 < imax) {
-          // select the (h+1)-th live position of row_L
+          // select the (h+1)-th live position of row_L, G independent words at a time
+          constexpr int G = R >= 16 ? 4 : 1;
           uint32_t cnt = 0, cw = 0, cb = 0;
-          for (;; ++cw) {
-            cb = rows[row_addr<CH>(tl, cw)];
-            const uint32_t pc = __popc(cb);
-            if (cnt + pc > h) break;
-            cnt += pc;
+          for (;; cw += G) {
+            uint32_t wv[G], pc[G], sg = 0;
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+              wv[j] = rows[row_addr<CH>(tl, G > 1 ? min(cw + j, nw - 1) : cw)];
+              pc[j] = (G == 1 || cw + j < nw) ? __popc(wv[j]) : 0u;
+              sg += pc[j];
+            }
+            if (cnt + sg > h) {
+#pragma unroll
+              for (int j = 0; j < G - 1; ++j) {
+                if (cnt + pc[0] > h) break;
+                cnt += pc[0];
+                ++cw;
+                pc[0] = pc[j + 1];
+                wv[0] = wv[j + 1];
+              }
+              cb = wv[0];
+              break;
+            }
+            cnt += sg;
           }
           uint32_t p = cw * 32 + __fns(cb, 0, (int)(h - cnt) + 1);
           out[0] = key_at(p);

@@ -96,6 +96,10 @@ class Context:
         """Pin the kernel class (tests use it to drive every class at small sizes)."""
         _check(N.lib().mf_context_set_option(self._h, N.MF_OPT_FORCE_CLASS, cls))
 
+    def pipeline_chunk(self, samples: int) -> None:
+        """Largest chunk of the host-buffer pipeline in samples (0 restores the default)."""
+        _check(N.lib().mf_context_set_option(self._h, N.MF_OPT_PIPELINE_CHUNK, samples))
+
     def last_launches(self) -> int:
         return int(N.lib().mf_context_last_launches(self._h))
 
