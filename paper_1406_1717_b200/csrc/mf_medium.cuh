@@ -204,7 +204,8 @@ __global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t
       {
         auto key_at = [&](uint32_t p) -> U {
           const uint32_t s = src[p];
-          return (s & 0x8000u) ? B[pad<PS>(s & 0x7FFF)].key() : A[pad<PS>(s)].key();
+          const E* blk = (s & 0x8000u) ? B : A;   // one load from the selected block
+          return blk[pad<PS>(s & 0x7FFFu)].key();
         };
 
         // walk: team lane L emits outputs [L*SR, L*SR + SR) of this unit
@@ -243,22 +244,25 @@ __global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t
             if (i0 + t < imax) {
               const uint32_t ab = rab[(t - 1) * CH + tl];
               const uint32_t a = ab & 0xFFFF, b = ab >> 16;
-              // Delete(A, i-1) and Undelete(B, i-1): clear / set one live bit each; the
-              // cached cursor word is authoritative for word cw, shared memory for the rest
-              if ((a >> 5) == cw) cb &= ~(1u << (a & 31)); else rows[row_addr<CH>(tl, a >> 5)] &= ~(1u << (a & 31));
-              if ((b >> 5) == cw) cb |= 1u << (b & 31); else rows[row_addr<CH>(tl, b >> 5)] |= 1u << (b & 31);
-              const bool up = (a == p) ? (b > p) : (a < p && b > p);
-              const bool down = (a == p) ? (b < p) : (a > p && b < p);
-              if (up) {
-                const uint32_t sh = (p & 31) + 1;
-                uint32_t m = sh < 32 ? cb & (0xFFFFFFFFu << sh) : 0u;
-                while (m == 0) { rows[row_addr<CH>(tl, cw)] = cb; ++cw; cb = rows[row_addr<CH>(tl, cw)]; m = cb; }
-                p = cw * 32 + __ffs(m) - 1;
-              } else if (down) {
-                uint32_t m = cb & ((1u << (p & 31)) - 1u);
-                while (m == 0) { rows[row_addr<CH>(tl, cw)] = cb; --cw; cb = rows[row_addr<CH>(tl, cw)]; m = cb; }
-                p = cw * 32 + 31 - __clz(m);
+              const uint32_t ba = 1u << (a & 31), bb = 1u << (b & 31);
+              // Delete(A, i-1) and Undelete(B, i-1), written through to the row in shared
+              // memory (fire-and-forget atomics, no divergence) and to the cached cursor word
+              atomicAnd(&rows[row_addr<CH>(tl, a >> 5)], ~ba);
+              atomicOr(&rows[row_addr<CH>(tl, b >> 5)], bb);
+              cb = sel((a >> 5) == cw, cb & ~ba, cb);
+              cb = sel((b >> 5) == cw, cb | bb, cb);
+              // the cursor moves up when the deletion is at or below it and the insertion above
+              const bool up = a <= p && b > p;
+              const bool down = a >= p && b < p;
+              const uint32_t sh = p & 31;
+              const uint32_t mu = cb & (0xFFFFFFFEu << sh);
+              const uint32_t md = cb & ((1u << sh) - 1u);
+              uint32_t m = sel(up, mu, md);
+              if ((up || down) && m == 0) {  // the next live position is in another word (rare)
+                const int dir = up ? 1 : -1;
+                do { cw += dir; cb = rows[row_addr<CH>(tl, cw)]; m = cb; } while (m == 0);
               }
+              p = sel(up, cw * 32 + __ffs(m) - 1, sel(down, cw * 32 + 31 - __clz(m), p));
               out[t] = key_at(p);
             }
           }
