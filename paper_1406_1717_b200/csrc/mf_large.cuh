@@ -120,7 +120,20 @@ __device__ __forceinline__ int merge_tile(E* s, const E* X, const E* Y, uint32_t
   const uint32_t a0 = sp.x, a1 = sp.y;   // merge-path splits, precomputed by ml_partition_*
   const uint32_t b0 = d0 - a0, b1 = d1 - a1;
   const uint32_t nx = a1 - a0, ny = b1 - b0;
-  for (uint32_t i = threadIdx.x; i < nx + ny; i += LNT) s[pad<LPS>(i)] = i < nx ? X[a0 + i] : Y[b0 + i - nx];
+  {  // stage the tile's inputs: all LR2 global loads in flight before the shared stores
+    E tmp[LR2];
+#pragma unroll
+    for (int j = 0; j < LR2; ++j) {
+      const uint32_t i = threadIdx.x + j * LNT;
+      const E* src = i < nx ? X + a0 + i : Y + b0 + (i - nx);
+      if (i < nx + ny) tmp[j] = ldg_elem(src);
+    }
+#pragma unroll
+    for (int j = 0; j < LR2; ++j) {
+      const uint32_t i = threadIdx.x + j * LNT;
+      if (i < nx + ny) s[pad<LPS>(i)] = tmp[j];
+    }
+  }
   __syncthreads();
   nx_out = nx;
   const int dd = threadIdx.x * LR2;
@@ -282,13 +295,22 @@ __global__ void __launch_bounds__(LNT, 4) ml_unit_merge(LargeGeom L, const Elem<
       uint2* slot = ro + (uint64_t)(idx & (L.CL - 1)) * C + (idx >> L.CLshift);  // transposed [t][c]
       if (srcB[r]) slot->y = q; else slot->x = q;
       const uint32_t sw = (dd + r) >> 10;                   // superword within the tile
-      atomicAdd(&hist[(sw * 2 + (srcB[r] ? 1 : 0)) * C + idx / L.CL], 1u);
+      atomicAdd(&hist[(sw * 2 + (srcB[r] ? 1 : 0)) * C + (idx >> L.CLshift)], 1u);
     }
   }
   __syncthreads();
   U* mko = mk + ug * L.nqp + d0;
   uint32_t* oo = org + ug * L.nqp + d0;
-  for (uint32_t i = threadIdx.x; i < d1 - d0; i += LNT) { mko[i] = sk[i]; oo[i] = so[i]; }
+  {  // 16-byte copies (d0 and the unit stride nqp are multiples of 32 elements)
+    constexpr uint32_t KV = 16 / sizeof(U);
+    const uint32_t nv = (d1 - d0) / 4, nk = (d1 - d0) / KV;
+    for (uint32_t i = threadIdx.x; i < nk; i += LNT)
+      reinterpret_cast<uint4*>(mko)[i] = reinterpret_cast<const uint4*>(sk)[i];
+    for (uint32_t i = threadIdx.x; i < nv; i += LNT)
+      reinterpret_cast<uint4*>(oo)[i] = reinterpret_cast<const uint4*>(so)[i];
+    for (uint32_t i = nk * KV + threadIdx.x; i < d1 - d0; i += LNT) mko[i] = sk[i];
+    for (uint32_t i = nv * 4 + threadIdx.x; i < d1 - d0; i += LNT) oo[i] = so[i];
+  }
   // live count of each superword at every chunk start c: A elements with chunk >= c plus
   // B elements with chunk < c.  One warp per superword; lanes scan 32 chunks at a time.
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -372,7 +394,13 @@ __global__ void __launch_bounds__(LNT) ml_walk(LargeGeom L, const typename Trait
   const uint2* rb = rab + ug * (uint64_t)L.C * L.CL + c;      // step t at rb[t * C]
   TV* y = reinterpret_cast<TV*>(g.y) + row * g.ld_y + u * k + i0;
 
-  uint32_t p = 0, cw = 0, cb = 0;
+  // The cursor's neighbourhood is a 64-position window: words cw0 and cw0+1 of the live set.
+  // When the cursor leaves it the window slides by one word (one live_word), so the cursor
+  // sits mid-window afterwards and small back-and-forth moves never recompute a word.
+  const uint32_t nwq = L.nqp / 32;                             // words per unit
+  auto word = [&](uint32_t w, uint32_t i) -> uint32_t { return w < nwq ? live_word(og, w, i, L.nq) : 0u; };
+  uint32_t p = 0, cw0 = 0;
+  uint64_t win = 0;
   if (active) {
     // select: superword S with prefix(S) <= h < prefix(S+1) (prefix of the live counts,
     // read 8 superwords at a time), then the words inside it
@@ -396,7 +424,7 @@ __global__ void __launch_bounds__(LNT) ml_walk(LargeGeom L, const typename Trait
       acc += s8;
     }
     uint32_t r = h - acc;
-    cw = S * 32;
+    uint32_t cw = S * 32, cb = 0;
     for (;; ++cw) {
       cb = live_word(og, cw, i0, L.nq);
       const uint32_t pc = __popc(cb);
@@ -404,6 +432,8 @@ __global__ void __launch_bounds__(LNT) ml_walk(LargeGeom L, const typename Trait
       r -= pc;
     }
     p = cw * 32 + __fns(cb, 0, (int)r + 1);
+    cw0 = cw;
+    win = (uint64_t)cb | ((uint64_t)word(cw + 1, i0) << 32);
   }
   const uint32_t my_n = active ? i1 - i0 : 0u;
   for (uint32_t t0 = 0; t0 < L.CL; t0 += 8) {
@@ -415,20 +445,27 @@ __global__ void __launch_bounds__(LNT) ml_walk(LargeGeom L, const typename Trait
         if (t > 0) {
           const uint2 ab = __ldg(rb + (uint64_t)(t - 1) * L.C);
           const uint32_t a = ab.x, b = ab.y;
-          if ((a >> 5) == cw) cb &= ~(1u << (a & 31));
-          if ((b >> 5) == cw) cb |= 1u << (b & 31);
-          const bool up = (a == p) ? (b > p) : (a < p && b > p);
-          const bool down = (a == p) ? (b < p) : (a > p && b < p);
-          if (up) {
-            const uint32_t sh = (p & 31) + 1;
-            uint32_t m = sh < 32 ? cb & (0xFFFFFFFFu << sh) : 0;
-            while (m == 0) { ++cw; cb = live_word(og, cw, i, L.nq); m = cb; }
-            p = cw * 32 + __ffs(m) - 1;
-          } else if (down) {
-            uint32_t m = cb & ((1u << (p & 31)) - 1u);
-            while (m == 0) { --cw; cb = live_word(og, cw, i, L.nq); m = cb; }
-            p = cw * 32 + 31 - __clz(m);
+          const uint32_t base = cw0 * 32;
+          const uint32_t oa = a - base, ob = b - base, off = p - base;   // window offsets
+          win &= ~(oa < 64 ? 1ull << oa : 0ull);
+          win |= ob < 64 ? 1ull << ob : 0ull;
+          const bool up = a <= p && b > p;
+          const bool down = a >= p && b < p;
+          uint64_t m = sel(up, (uint64_t)(win & (0xFFFFFFFFFFFFFFFEull << off)), (uint64_t)(win & ((1ull << off) - 1ull)));
+          if ((up || down) && m == 0) {  // slide the window one word at a time (rare)
+            do {
+              if (up) {
+                ++cw0;
+                win = (win >> 32) | ((uint64_t)word(cw0 + 1, i) << 32);
+                m = win & 0xFFFFFFFF00000000ull;
+              } else {
+                --cw0;
+                win = (win << 32) | word(cw0, i);
+                m = win & 0xFFFFFFFFull;
+              }
+            } while (m == 0);
           }
+          p = sel(up, cw0 * 32 + __ffsll((long long)m) - 1, sel(down, cw0 * 32 + 63 - __clzll((long long)m), p));
         }
         stage[lane * 9 + tt] = __ldg(mkg + p);
       }

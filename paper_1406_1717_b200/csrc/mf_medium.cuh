@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t
           amask |= (uint64_t)(valid && takeA) << r;
           ia += takeA;
           ib += !takeA;
-          const E nv = takeA ? A[pad<PS>(min(ia, K - 1))] : B[pad<PS>(min(ib, K - 1))];
+          const E nv = (takeA ? A : B)[pad<PS>(min(sel(takeA, (uint32_t)ia, (uint32_t)ib), (uint32_t)K - 1))];
           ea = E::select(takeA, nv, ea);
           eb = E::select(takeA, eb, nv);
         }

@@ -95,6 +95,17 @@ __device__ __forceinline__ Elem<uint64_t> shfl_xor(const Elem<uint64_t>& e, int 
   Elem<uint64_t> r; r.k = __shfl_xor_sync(0xFFFFFFFFu, e.k, m); r.i = __shfl_xor_sync(0xFFFFFFFFu, e.i, m); return r;
 }
 
+// read-only (non-coherent cache path) element loads
+__device__ __forceinline__ Elem<uint32_t> ldg_elem(const Elem<uint32_t>* p) {
+  Elem<uint32_t> r; r.v = __ldg(reinterpret_cast<const unsigned long long*>(&p->v)); return r;
+}
+__device__ __forceinline__ Elem<uint64_t> ldg_elem(const Elem<uint64_t>* p) {
+  Elem<uint64_t> r;
+  r.k = __ldg(reinterpret_cast<const unsigned long long*>(&p->k));
+  r.i = __ldg(&p->i);
+  return r;
+}
+
 template <int K, int I, typename E>
 __device__ __forceinline__ void net_apply(E* v) {
   if constexpr (I < OEM<K>::net.n) {
