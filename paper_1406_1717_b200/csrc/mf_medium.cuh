@@ -47,7 +47,7 @@ struct MediumCfg {
   // padded element index: blocked per-lane writes hit distinct banks (8-byte elements)
   static constexpr int PS = pad_shift<RS>();
   static constexpr int SLOT = BS + (BS >> PS) + 1;
-  static constexpr size_t sz_sorted = sizeof(E) * SLOT * (W + 1);
+  static constexpr size_t sz_sorted = (sizeof(E) * SLOT * (W + 1) + 15) / 16 * 16;
   static constexpr size_t sz_src = sizeof(uint16_t) * 2 * BS;  // merged pos -> (isB, sorted pos)
   static constexpr size_t sz_rab = sizeof(uint32_t) * BS;      // RA | RB << 16, transposed [t][lane]
   static constexpr size_t sz_rows_bits = sizeof(uint32_t) * NW * CH;
@@ -135,14 +135,22 @@ __global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t
       const E* A = slot(team);
       const E* B = slot(team + 1);
 
-      for (uint32_t i = tl; i < NW * CH; i += TL) rows[i] = 0;
-      for (uint32_t w = tl; w < NW; w += TL) abits[w] = 0;
+      constexpr int PL = 2 * R / WP;             // merged positions per team lane (divides 32)
+      constexpr bool OWN = PL == 32;             // each lane owns one whole word of every row
+      {
+        uint4* r4 = reinterpret_cast<uint4*>(rows);
+        for (uint32_t i = tl; i < NW * CH / 4; i += TL) r4[i] = make_uint4(0, 0, 0, 0);
+        if constexpr (!OWN)
+          for (uint32_t w = tl; w < NW; w += TL) abits[w] = 0;
+      }
       team_sync();
 
-      // merge path: team lane owns merged positions [tl*PL, tl*PL + PL); branch-free steps
+      // merge path: team lane owns merged positions [tl*PL, tl*PL + PL), all inside word
+      // w0 = d/32 of every row; branch-free steps
+      const int d = tl * PL;
+      const uint32_t w0 = (uint32_t)d >> 5, bo = (uint32_t)d & 31;
+      uint32_t amask = 0;                        // A-side bits of this lane's positions (word w0)
       {
-        constexpr int PL = 2 * R / WP;
-        const int d = tl * PL;
         const int K = (int)k;
         int lo = d > K ? d - K : 0, hi = d < K ? d : K;
         if (d >= (int)nq) lo = hi = 0;
@@ -152,45 +160,36 @@ __global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t
         }
         int ia = lo, ib = d - lo;
         E ea = A[pad<PS>(min(ia, K - 1))], eb = B[pad<PS>(min(max(ib, 0), K - 1))];
-        uint64_t amask = 0;                      // A-side bits of this lane's PL positions
         uint16_t* rab16 = reinterpret_cast<uint16_t*>(rab);
-#pragma unroll 4
+        uint32_t* rcol = rows + w0 * CH;         // row_addr<CH>(c, w0) = rcol[c ^ xr]
+        const uint32_t xr = w0 & (CH - 1);
+        constexpr int LSR = __builtin_ctz(SR);
+#pragma unroll 8
         for (int r = 0; r < PL; ++r) {
           const int q = d + r;
           const bool valid = q < (int)nq;
           const bool takeA = (ib >= K) || (ia < K && ea.key() <= eb.key());
           const uint32_t idx = sel(takeA, ea.idx(), eb.idx());
-          const uint32_t c = idx / SR;           // owning team lane (chunk) of this element
+          const uint32_t c = idx >> LSR;         // owning team lane (chunk) of this element
+          const uint32_t bit = 1u << (bo + r);
           if (valid) {
-            atomicOr(&rows[row_addr<CH>(c, q >> 5)], 1u << (q & 31));
+            atomicOr(&rcol[c ^ xr], bit);
             src[q] = (uint16_t)sel(takeA, (uint32_t)ia, 0x8000u | (uint32_t)ib);
-            rab16[2 * ((idx % SR) * CH + c) + (takeA ? 0 : 1)] = (uint16_t)q;
+            rab16[2 * ((idx & (SR - 1)) * CH + c) + (takeA ? 0 : 1)] = (uint16_t)q;
           }
-          amask |= (uint64_t)(valid && takeA) << r;
+          amask |= (valid && takeA) ? bit : 0u;
           ia += takeA;
           ib += !takeA;
           const E nv = (takeA ? A : B)[pad<PS>(min(sel(takeA, (uint32_t)ia, (uint32_t)ib), (uint32_t)K - 1))];
           ea = E::select(takeA, nv, ea);
           eb = E::select(takeA, eb, nv);
         }
-        // fold the lane's A bits into abits (PL <= 64 positions, at most 3 words)
-        if (d < (int)nq) {
-#pragma unroll
-          for (int w0 = 0; w0 < (PL + 31) / 32 + 1; ++w0) {
-            const int wq = (d >> 5) + w0;
-            const int sh = wq * 32 - d;          // bit offset of word wq in amask
-            uint32_t bits;
-            if (sh >= 64 || sh <= -32) bits = 0;
-            else if (sh >= 0) bits = (uint32_t)(amask >> sh);
-            else bits = (uint32_t)(amask << (-sh));
-            if (bits) atomicOr(&abits[wq], bits);
-          }
-        }
+        if constexpr (!OWN)
+          if (d < (int)nq) atomicOr(&abits[w0], amask);
       }
-      team_sync();
-      // XOR prefix over chunks: row_L = A_bits ^ (toggles of chunks < L)
-      for (uint32_t w = tl; w < nw; w += TL) {
-        uint32_t acc = abits[w];
+      // XOR prefix over chunks: row_L = A_bits ^ (toggles of chunks < L).  A lane that owns
+      // its word wrote every toggle of it itself, so it needs no barrier before its prefix.
+      auto prefix = [&](uint32_t w, uint32_t acc) {
 #pragma unroll 8
         for (uint32_t L = 0; L < (uint32_t)CH; ++L) {
           const uint32_t a = row_addr<CH>(L, w);
@@ -198,6 +197,12 @@ __global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t
           rows[a] = acc;
           acc ^= dlt;
         }
+      };
+      if constexpr (OWN) {
+        if (w0 < nw) prefix(w0, amask);
+      } else {
+        team_sync();
+        for (uint32_t w = tl; w < nw; w += TL) prefix(w, abits[w]);
       }
       team_sync();
 
