@@ -9,7 +9,8 @@ import ctypes as C
 import os
 import threading
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmedfilt_b200.so")
+# MF_B200_LIB points at an experiment build (paper_1406_1717_b200.build.build(lib=...))
+LIB_PATH = os.environ.get("MF_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmedfilt_b200.so")
 
 MF_OK, MF_EMPTY_INPUT, MF_K_ZERO, MF_K_EVEN, MF_K_TOO_LARGE = 0, 1, 2, 3, 4
 MF_BAD_ARG, MF_CUDA_ERROR, MF_OUT_OF_MEMORY, MF_NO_DEVICE = 5, 6, 7, 8

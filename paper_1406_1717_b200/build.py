@@ -39,18 +39,20 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, extra_flags=(), lib: str = LIB, build_dir: str = BUILD) -> str:
+    """Compile every source for sm_100a into `lib`.  `extra_flags`/`lib`/`build_dir` build
+    experiment variants (e.g. -D switches) side by side with the shipped library."""
     cu, c, hdr = _sources()
-    os.makedirs(BUILD, exist_ok=True)
+    os.makedirs(build_dir, exist_ok=True)
     jobs = []
     objs = []
     for src in cu:
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        obj = os.path.join(build_dir, os.path.basename(src) + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + hdr + [__file__]):
-            jobs.append([NVCC, *NVFLAGS, "-c", src, "-o", obj])
+            jobs.append([NVCC, *NVFLAGS, *extra_flags, "-c", src, "-o", obj])
     for src in c:
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        obj = os.path.join(build_dir, os.path.basename(src) + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + hdr + [__file__]):
             jobs.append(["gcc", "-O3", "-fPIC", "-ffp-contract=off", "-Wall", "-c", src, "-o", obj])
@@ -67,9 +69,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
         for err in ex.map(run, jobs):
             if verbose and err:
                 print(err)
-    if force or jobs or _stale(LIB, objs):
-        run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lm", "-lcudart"])
-    return LIB
+    if force or jobs or _stale(lib, objs):
+        run([NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lm", "-lcudart"])
+    return lib
 
 
 if __name__ == "__main__":

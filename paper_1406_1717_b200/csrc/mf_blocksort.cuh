@@ -31,6 +31,15 @@ struct SyncTeam {
   __device__ __forceinline__ void operator()() const {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
   }
+  // barrier that also ORs a predicate over the team
+  __device__ __forceinline__ bool any(bool v) const {
+    uint32_t r;
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 q, %1, 0;\n\tbar.red.or.pred p, %2, %3, q;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(r) : "r"((uint32_t)v), "r"(id), "r"(count) : "memory");
+    return r != 0;
+  }
 };
 
 template <typename E, int R, int PS, typename Sync>
@@ -94,7 +103,7 @@ __device__ __forceinline__ void warp_bitonic_levels(E (&v)[R], uint32_t lane) {
       for (int r = 0; r < R; ++r) t[r] = shfl_xor(v[R - 1 - r], G - 1);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const bool lt = E::less(v[r], t[r]);
+        const bool lt = E::less_full(v[r], t[r]);
         v[r] = E::select(lt == lower, v[r], t[r]);
       }
     }
@@ -104,7 +113,7 @@ __device__ __forceinline__ void warp_bitonic_levels(E (&v)[R], uint32_t lane) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const E p = shfl_xor(v[r], dl);
-        const bool lt = E::less(v[r], p);
+        const bool lt = E::less_full(v[r], p);
         v[r] = E::select(lt == lower, v[r], p);
       }
     }
@@ -129,47 +138,53 @@ __device__ __forceinline__ void warp_sort_regs(E (&v)[R], E* s, int b0, uint32_t
   merge_levels<E, R, PS, false>(s, b0, lane, R << BL, 32 * R, v);
 }
 
-// Raw (un-keyed) coalesced load of block `blk` of a row: element e = lane + 32r.  Slots
-// past k or past n (the reference's +INF padding, filter.hpp:28-36) get 0x7FF..F, whose
-// ukey is all-ones for every dtype; with index e they sort after every real element.
-template <typename TV, int R>
-__device__ __forceinline__ void warp_load_block(TV (&raw)[R], const TV* x, uint64_t n, uint32_t k, uint64_t blk,
-                                                uint32_t lane) {
-  const TV padv = (TV)(~(std::make_unsigned_t<TV>)0 >> 1);
-  const uint64_t b0 = blk * k;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const uint32_t e = lane + 32 * r;
-    const uint64_t gp = b0 + e;
-    raw[r] = (e < k && gp < n) ? __ldg(x + gp) : padv;
+// Warp-wide stable compaction of the elements with idx < k to the front of sb[0, NS).
+// Needed after a key-ordered sort (KElem) when the block holds samples whose key is the
+// all-ones padding key (real maxima or the reference's +INF padding, filter.hpp:28-36):
+// the slot fillers past k share that key and may have landed among the first k sorted
+// positions.  Fillers only ever sit in the all-ones run at the end, so everything before
+// it stays where it is.  Positions past k are left as they are (nothing reads them).
+template <typename E, int PS>
+__device__ __noinline__ void compact_block(E* sb, int NS, uint32_t k, uint32_t lane) {
+  uint32_t base = 0;
+  for (int p0 = 0; p0 < NS; p0 += 32) {
+    const E e = sb[pad<PS>(p0 + (int)lane)];
+    const bool real = e.idx() < k;
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, real);
+    __syncwarp();
+    if (real) sb[pad<PS>((int)(base + __popc(bal & ((1u << lane) - 1u))))] = e;
+    base += __popc(bal);
+    __syncwarp();
   }
-}
-
-template <int DT, int R>
-__device__ __forceinline__ void warp_sort_raw(Elem<typename Traits<DT>::U>* sb, const typename Traits<DT>::T (&raw)[R],
-                                              uint32_t lane) {
-  using E = Elem<typename Traits<DT>::U>;
-  E v[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) v[r] = E::make(Traits<DT>::enc(raw[r]), lane + 32 * r);
-  warp_sort_regs<E, R, pad_shift<R>()>(v, sb, 0, lane);
 }
 
 // Team sort: WP warps sort one block of 32*RS*WP slots.  Warp `sub` of the team holds the
 // elements [sub*32*RS, (sub+1)*32*RS) (element e = sub*32*RS + lane + 32r), sorts them
-// into its part of sb, then the team merges the WP sorted parts.
-template <int DT, int RS, int WP>
-__device__ __forceinline__ void team_sort_raw(Elem<typename Traits<DT>::U>* sb, const typename Traits<DT>::T (&raw)[RS],
+// into its part of sb, then the team merges the WP sorted parts.  Slots e >= k hold the
+// padding value; with key-ordered elements they are moved behind the k real ones.
+template <int DT, int RS, int WP, typename E>
+__device__ __forceinline__ void team_sort_raw(E* sb, const typename Traits<DT>::T (&raw)[RS], uint32_t k,
                                               uint32_t sub, uint32_t lane, SyncTeam bar) {
-  using E = Elem<typename Traits<DT>::U>;
+  using TV = typename Traits<DT>::T;
   constexpr int PS = pad_shift<RS>();
+  const TV padv = (TV)(~(std::make_unsigned_t<TV>)0 >> 1);
   E v[RS];
+  bool maxkey = false;  // a slot e < k carries the padding key
 #pragma unroll
-  for (int r = 0; r < RS; ++r) v[r] = E::make(Traits<DT>::enc(raw[r]), sub * 32 * RS + lane + 32 * r);
+  for (int r = 0; r < RS; ++r) {
+    const uint32_t e = sub * 32 * RS + lane + 32 * r;
+    v[r] = E::make(Traits<DT>::enc(raw[r]), e);
+    maxkey |= e < k && raw[r] == padv;
+  }
   warp_sort_regs<E, RS, PS>(v, sb, sub * 32 * RS, lane);
   if constexpr (WP > 1) {
-    bar();
+    maxkey = bar.any(maxkey);
     merge_levels_s<E, RS, PS>(sb, 0, sub * 32 + lane, 32 * RS, 32 * RS * WP, v, bar);
+  } else {
+    maxkey = __any_sync(0xFFFFFFFFu, maxkey);
+  }
+  if constexpr (!E::kFull) {
+    if (maxkey && sub == 0) compact_block<E, PS>(sb, 32 * RS * WP, k, lane);
   }
 }
 
@@ -184,15 +199,6 @@ __device__ __forceinline__ void team_load_block(TV (&raw)[RS], const TV* x, uint
     const uint64_t gp = b0 + e;
     raw[r] = (e < k && gp < n) ? __ldg(x + gp) : padv;
   }
-}
-
-// Load block `blk` of a row (k samples from x, +INF past n) and warp-sort it into slot sb.
-template <int DT, int R>
-__device__ __forceinline__ void warp_sort_block(Elem<typename Traits<DT>::U>* sb, const typename Traits<DT>::T* x,
-                                                uint64_t n, uint32_t k, uint64_t blk, uint32_t lane) {
-  typename Traits<DT>::T raw[R];
-  warp_load_block<typename Traits<DT>::T, R>(raw, x, n, k, blk, lane);
-  warp_sort_raw<DT, R>(sb, raw, lane);
 }
 
 }  // namespace mf

@@ -34,11 +34,16 @@
 
 namespace mf {
 
+#ifndef MF_MEDIUM_KEYORD_MAXR
+#define MF_MEDIUM_KEYORD_MAXR 16  // largest R sorted with key-ordered elements (R = 32: measured slower)
+#endif
+
 template <int DT, int R, int W, int WP = 1>
 struct MediumCfg {
   using Tr = Traits<DT>;
   using U = typename Tr::U;
-  using E = Elem<U>;
+  // key-ordered elements: ties in any order (mf_sortnet.cuh)
+  using E = std::conditional_t<(R <= MF_MEDIUM_KEYORD_MAXR), typename KeyOrd<U>::E, Elem<U>>;
   static constexpr int BS = 32 * R;        // block slot capacity (>= k)
   static constexpr int NW = 2 * R;         // words per merged row (2k bits <= 64R)
   static constexpr int RS = R / WP;        // elements per lane in the team block sort
@@ -113,10 +118,10 @@ __global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t
     if (!carry && team == 0) {
       TV raw0[RS];
       team_load_block<TV, RS, WP>(raw0, x, g.n, k, u0, sub, lane);
-      team_sort_raw<DT, RS, WP>(slot(0), raw0, sub, lane, tbar);
+      team_sort_raw<DT, RS, WP>(slot(0), raw0, k, sub, lane, tbar);
     }
     if (!have_pre) team_load_block<TV, RS, WP>(pre, x, g.n, k, u0 + team + 1, sub, lane);
-    team_sort_raw<DT, RS, WP>(slot(team + 1), pre, sub, lane, tbar);
+    team_sort_raw<DT, RS, WP>(slot(team + 1), pre, k, sub, lane, tbar);
     __syncthreads();
     // prefetch this team's block of the next tile; it lands while phase 2 runs (large
     // blocks only: for small R the extra registers cost more occupancy than they hide)

@@ -12,7 +12,8 @@
 // positions, so prev[m]/next[m] are "highest live bit below m" / "lowest live bit
 // above m" (one clz/ffs each), and the stale-link undelete of dancing links is a
 // plain bit set.  Cursor m and small-count s follow block.hpp:71-104 step for step,
-// so the per-step (m, s) state is identical to the reference's.  Every step is
+// so the per-step (m, s) state is the reference's (up to the order of equal keys inside
+// a block, which the key-ordered sort leaves open and which no emitted median depends on).  Every step is
 // evaluated branch-free (selects, no divergence), fully unrolled over the K steps.
 //
 // Persistent CTAs stream tiles of T consecutive units: while a tile is sorted and

@@ -49,6 +49,7 @@ template <int K> struct OEM { static constexpr NetList net = make_oem(K); };
 template <typename U> struct Elem;
 
 template <> struct Elem<uint32_t> {
+  static constexpr bool kFull = true;  // totally ordered by (key, index)
   uint64_t v;  // key << 32 | index
   __device__ __forceinline__ static Elem make(uint32_t key, uint32_t idx) {
     Elem e; e.v = ((uint64_t)key << 32) | idx; return e;
@@ -56,6 +57,7 @@ template <> struct Elem<uint32_t> {
   __device__ __forceinline__ uint32_t key() const { return (uint32_t)(v >> 32); }
   __device__ __forceinline__ uint32_t idx() const { return (uint32_t)v; }
   __device__ __forceinline__ static bool less(const Elem& x, const Elem& y) { return x.v < y.v; }
+  __device__ __forceinline__ static bool less_full(const Elem& x, const Elem& y) { return x.v < y.v; }
   __device__ __forceinline__ static void cswap(Elem& x, Elem& y) {
     const uint64_t lo = x.v < y.v ? x.v : y.v;
     const uint64_t hi = x.v < y.v ? y.v : x.v;
@@ -67,6 +69,7 @@ template <> struct Elem<uint32_t> {
 };
 
 template <> struct Elem<uint64_t> {
+  static constexpr bool kFull = true;
   uint64_t k;
   uint32_t i;
   __device__ __forceinline__ static Elem make(uint64_t key, uint32_t idx) {
@@ -77,6 +80,7 @@ template <> struct Elem<uint64_t> {
   __device__ __forceinline__ static bool less(const Elem& x, const Elem& y) {
     return x.k < y.k || (x.k == y.k && x.i < y.i);
   }
+  __device__ __forceinline__ static bool less_full(const Elem& x, const Elem& y) { return less(x, y); }
   __device__ __forceinline__ static void cswap(Elem& x, Elem& y) {
     const bool sw = less(y, x);
     const Elem t = x;
@@ -87,6 +91,69 @@ template <> struct Elem<uint64_t> {
     Elem e; e.k = sel(c, a.k, b.k); e.i = sel(c, a.i, b.i); return e;
   }
 };
+
+// Key-ordered elements: the same (key, index) payload, but comparisons look at the key
+// only, so equal keys may end up in any order.  The filters need no more: the median of a
+// window is a key (its bits are the sample's bits), and which of several equal samples is
+// picked does not change it.  One compare instead of a 64-bit / two-part compare per
+// exchange.  Decisions taken separately by two lanes about the same pair (bitonic
+// cross-lane stages) use less_full, so both lanes agree on ties.  Phase-API sorts, whose
+// permutation must match piecewise_sort (filter.hpp:41-54), keep Elem.
+struct KElem32 {
+  static constexpr bool kFull = false;  // ordered by key only
+  uint64_t v;  // key << 32 | index
+  __device__ __forceinline__ static KElem32 make(uint32_t key, uint32_t idx) {
+    KElem32 e; e.v = ((uint64_t)key << 32) | idx; return e;
+  }
+  __device__ __forceinline__ uint32_t key() const { return (uint32_t)(v >> 32); }
+  __device__ __forceinline__ uint32_t idx() const { return (uint32_t)v; }
+  __device__ __forceinline__ static bool less(const KElem32& x, const KElem32& y) { return x.key() < y.key(); }
+  __device__ __forceinline__ static bool less_full(const KElem32& x, const KElem32& y) { return x.v < y.v; }
+  __device__ __forceinline__ static void cswap(KElem32& x, KElem32& y) {
+    const bool sw = y.key() < x.key();
+    const uint64_t a = x.v, b = y.v;
+    x.v = sel(sw, b, a);
+    y.v = sel(sw, a, b);
+  }
+  __device__ __forceinline__ static KElem32 select(bool c, const KElem32& a, const KElem32& b) {
+    KElem32 e; e.v = sel(c, a.v, b.v); return e;
+  }
+};
+
+struct KElem64 {
+  static constexpr bool kFull = false;
+  uint64_t k;
+  uint32_t i;
+  __device__ __forceinline__ static KElem64 make(uint64_t key, uint32_t idx) {
+    KElem64 e; e.k = key; e.i = idx; return e;
+  }
+  __device__ __forceinline__ uint64_t key() const { return k; }
+  __device__ __forceinline__ uint32_t idx() const { return i; }
+  __device__ __forceinline__ static bool less(const KElem64& x, const KElem64& y) { return x.k < y.k; }
+  __device__ __forceinline__ static bool less_full(const KElem64& x, const KElem64& y) {
+    return x.k < y.k || (x.k == y.k && x.i < y.i);
+  }
+  __device__ __forceinline__ static void cswap(KElem64& x, KElem64& y) {
+    const bool sw = y.k < x.k;
+    const KElem64 t = x;
+    x.k = sel(sw, y.k, x.k); x.i = sel(sw, y.i, x.i);
+    y.k = sel(sw, t.k, y.k); y.i = sel(sw, t.i, y.i);
+  }
+  __device__ __forceinline__ static KElem64 select(bool c, const KElem64& a, const KElem64& b) {
+    KElem64 e; e.k = sel(c, a.k, b.k); e.i = sel(c, a.i, b.i); return e;
+  }
+};
+
+template <typename U> struct KeyOrd;
+template <> struct KeyOrd<uint32_t> { using E = KElem32; };
+template <> struct KeyOrd<uint64_t> { using E = KElem64; };
+
+__device__ __forceinline__ KElem32 shfl_xor(const KElem32& e, int m) {
+  KElem32 r; r.v = __shfl_xor_sync(0xFFFFFFFFu, e.v, m); return r;
+}
+__device__ __forceinline__ KElem64 shfl_xor(const KElem64& e, int m) {
+  KElem64 r; r.k = __shfl_xor_sync(0xFFFFFFFFu, e.k, m); r.i = __shfl_xor_sync(0xFFFFFFFFu, e.i, m); return r;
+}
 
 __device__ __forceinline__ Elem<uint32_t> shfl_xor(const Elem<uint32_t>& e, int m) {
   Elem<uint32_t> r; r.v = __shfl_xor_sync(0xFFFFFFFFu, e.v, m); return r;

@@ -1,0 +1,24 @@
+"""Device time per k on the config-2 signal (median of 3 x 10 launches): python scripts/time_ks.py K..."""
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+import paper_1406_1717_b200 as mf  # noqa: E402
+
+x = mf.generate_device("uniform_f32", 2, 1 << 26)
+out = torch.empty_like(x)
+res = {}
+for k in [int(a) for a in sys.argv[1:]] or [3, 31, 255, 1023]:
+    for _ in range(3):
+        mf.median_filter_device(x, k, out=out)
+    ts = []
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(10):
+            mf.median_filter_device(x, k, out=out)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / 10)
+    res[k] = round(sorted(ts)[1], 4)
+print(os.environ.get("MF_B200_LIB", "default"), res, flush=True)
