@@ -126,10 +126,12 @@ __device__ __forceinline__ void warp_bitonic_levels(E (&v)[R], uint32_t lane) {
   }
 }
 
-template <typename E, int R, int PS>
+// Warp sort: register network per lane, then BLV register bitonic levels (shuffles; 5 =
+// the whole warp), then shared-memory merge-path levels up to 32R.  16-byte elements skip
+// the bitonic levels (measured: no gain for 64-bit keys).
+template <typename E, int R, int PS, int BLV>
 __device__ __forceinline__ void warp_sort_regs(E (&v)[R], E* s, int b0, uint32_t lane) {
-  // register bitonic levels before the smem merges (measured: 64-bit keys gain nothing)
-  constexpr int BL = sizeof(E) > 8 ? 0 : (R >= 16 ? 2 : 4);
+  constexpr int BL = sizeof(E) > 8 ? 0 : BLV;
   sort_regs<R>(v);
   warp_bitonic_levels<E, R, BL>(v, lane);
 #pragma unroll
@@ -162,7 +164,7 @@ __device__ __noinline__ void compact_block(E* sb, int NS, uint32_t k, uint32_t l
 // elements [sub*32*RS, (sub+1)*32*RS) (element e = sub*32*RS + lane + 32r), sorts them
 // into its part of sb, then the team merges the WP sorted parts.  Slots e >= k hold the
 // padding value; with key-ordered elements they are moved behind the k real ones.
-template <int DT, int RS, int WP, typename E>
+template <int DT, int RS, int WP, int BL, typename E>
 __device__ __forceinline__ void team_sort_raw(E* sb, const typename Traits<DT>::T (&raw)[RS], uint32_t k,
                                               uint32_t sub, uint32_t lane, SyncTeam bar) {
   using TV = typename Traits<DT>::T;
@@ -176,7 +178,7 @@ __device__ __forceinline__ void team_sort_raw(E* sb, const typename Traits<DT>::
     v[r] = E::make(Traits<DT>::enc(raw[r]), e);
     maxkey |= e < k && raw[r] == padv;
   }
-  warp_sort_regs<E, RS, PS>(v, sb, sub * 32 * RS, lane);
+  warp_sort_regs<E, RS, PS, BL>(v, sb, sub * 32 * RS, lane);
   if constexpr (WP > 1) {
     maxkey = bar.any(maxkey);
     merge_levels_s<E, RS, PS>(sb, 0, sub * 32 + lane, 32 * RS, 32 * RS * WP, v, bar);

@@ -84,7 +84,10 @@ __global__ void __launch_bounds__(LNT, 3) ml_tile_sort(LargeGeom L, Elem<typenam
     const U key = (e < k && gp < g.n) ? Tr::enc(__ldg(x + gp)) : UMax<U>::v;
     v[r] = E::make(key, e);
   }
-  warp_sort_regs<E, R, PS>(v, s, warp * 32 * R, lane);
+#ifndef MF_BL_LARGE
+#define MF_BL_LARGE 2  // bitonic register levels of the tile sort (experiments)
+#endif
+  warp_sort_regs<E, R, PS, MF_BL_LARGE>(v, s, warp * 32 * R, lane);
   __syncthreads();
   merge_levels<E, R, PS, true>(s, 0, threadIdx.x, 32 * R, TS, v);
   const uint32_t len = min((uint32_t)TS, k - t * TS);

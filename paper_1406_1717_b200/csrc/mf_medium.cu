@@ -10,7 +10,13 @@ namespace {
 // smaller R has a smaller footprint and gets more warps.
 template <int DT, int R> struct WarpsFor {
   static constexpr bool wide = sizeof(typename Traits<DT>::U) == 8;
-  static constexpr int value = R >= 32 ? 2 : (R >= 16 ? 4 : 8);
+#ifndef MF_W_R16
+#define MF_W_R16 8  // teams per CTA for R = 16 (experiments)
+#endif
+#ifndef MF_W_R8
+#define MF_W_R8 8   // ... for R <= 8
+#endif
+  static constexpr int value = R >= 32 ? 2 : (R >= 16 ? MF_W_R16 : MF_W_R8);
 };
 
 template <int DT, int R>

@@ -49,6 +49,13 @@ struct MediumCfg {
   static constexpr int RS = R / WP;        // elements per lane in the team block sort
   static constexpr int CH = 32 * WP;       // walk chunks per pair (one per team lane)
   static constexpr int SR = R / WP;        // steps per chunk
+#ifndef MF_BL_TEAM
+#define MF_BL_TEAM 3  // register bitonic levels of the warp sorts in 2-warp teams (experiments)
+#endif
+#ifndef MF_BL_WARP
+#define MF_BL_WARP 5  // ... in 1-warp teams (5: the whole block in registers)
+#endif
+  static constexpr int BL = WP > 1 ? MF_BL_TEAM : MF_BL_WARP;
   // padded element index: blocked per-lane writes hit distinct banks (8-byte elements)
   static constexpr int PS = pad_shift<RS>();
   static constexpr int SLOT = BS + (BS >> PS) + 1;
@@ -118,10 +125,10 @@ __global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t
     if (!carry && team == 0) {
       TV raw0[RS];
       team_load_block<TV, RS, WP>(raw0, x, g.n, k, u0, sub, lane);
-      team_sort_raw<DT, RS, WP>(slot(0), raw0, k, sub, lane, tbar);
+      team_sort_raw<DT, RS, WP, C::BL>(slot(0), raw0, k, sub, lane, tbar);
     }
     if (!have_pre) team_load_block<TV, RS, WP>(pre, x, g.n, k, u0 + team + 1, sub, lane);
-    team_sort_raw<DT, RS, WP>(slot(team + 1), pre, k, sub, lane, tbar);
+    team_sort_raw<DT, RS, WP, C::BL>(slot(team + 1), pre, k, sub, lane, tbar);
     __syncthreads();
     // prefetch this team's block of the next tile; it lands while phase 2 runs (large
     // blocks only: for small R the extra registers cost more occupancy than they hide)
