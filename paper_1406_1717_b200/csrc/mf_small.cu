@@ -7,10 +7,9 @@
 namespace mf {
 
 namespace {
-constexpr int kSmallThreads = 128;
-
 template <int DT, int K>
 cudaError_t launch_k(const Geom& g, cudaStream_t s) {
+  constexpr int kSmallThreads = SmallShape<DT, K>::T;
   using C = SmallCfg<DT, K, kSmallThreads>;
   auto kern = mf_small_kernel<DT, K, kSmallThreads>;
   static int resident = 0;  // CTAs per SM (per process; the attribute is idempotent)

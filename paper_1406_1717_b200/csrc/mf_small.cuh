@@ -28,14 +28,21 @@
 
 namespace mf {
 
-template <int K> struct UnitsPerThread { static constexpr int value = K <= 7 ? 4 : (K <= 15 ? 2 : 1); };
+// Tile shape by (key width, k): threads per CTA and units (block pairs) per thread per
+// tile, measured on config 2 (f32, 2^26 samples) for every odd k <= 31.  8-byte keys keep
+// 128 threads so that two tiles of input still fit the shared-memory budget.
+template <int DT, int K> struct SmallShape {
+  static constexpr bool wide = sizeof(typename Traits<DT>::U) == 8;
+  static constexpr int T = wide ? 128 : (K <= 5 ? 256 : K <= 7 ? 512 : K <= 23 ? 256 : 512);
+  static constexpr int UPT = wide ? (K <= 7 ? 4 : K <= 15 ? 2 : 1) : (K <= 5 ? 4 : K <= 11 ? 2 : 1);
+};
 
 template <int DT, int K, int T>
 struct SmallCfg {
   using Tr = Traits<DT>;
   using U = typename Tr::U;
   static constexpr int H = (K - 1) / 2;
-  static constexpr int UPT = UnitsPerThread<K>::value;  // units (block pairs) per thread per tile
+  static constexpr int UPT = SmallShape<DT, K>::UPT;  // units (block pairs) per thread per tile
   static constexpr int TU = T * UPT;                    // units per tile
   static constexpr int NB = TU + 1;                     // blocks (columns) per tile
   static constexpr int SC = TU + 32;                    // column stride: >= NB, a multiple of 32
