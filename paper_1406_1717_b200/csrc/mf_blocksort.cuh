@@ -190,6 +190,107 @@ __device__ __forceinline__ void team_sort_raw(E* sb, const typename Traits<DT>::
   }
 }
 
+// ---- key-only team sort (32-bit keys) -------------------------------------------------
+// The sorting network moves bare 32-bit keys: a compare-exchange is two min/max ops
+// (VIMNMX), a cross-lane stage one shuffle and a lane-directed min/max, where carrying the
+// index would cost a compare and four selects per exchange on the ALU pipe (the medium
+// kernel's limiter).  The permutation is recovered afterwards: each element's sorted
+// position is the number of smaller keys (a branch-free lower-bound search in the sorted
+// keys of every warp of the team) plus a tie slot claimed with a shared atomic, so equal
+// keys take distinct consecutive positions in some order -- the key order the medium
+// kernel needs (mf_sortnet.cuh, KElem32).  Slot fillers (e >= k) claim nothing, so the k
+// real elements (virtual +INF padding included, filter.hpp:28-36) fill positions [0, k).
+struct KeyU32 {
+  uint32_t v;
+  __device__ __forceinline__ static void cswap(KeyU32& x, KeyU32& y) {
+    const uint32_t lo = min(x.v, y.v), hi = max(x.v, y.v);
+    x.v = lo; y.v = hi;
+  }
+};
+
+// register bitonic levels on bare keys (layout as warp_bitonic_levels)
+template <int R, int LEVELS>
+__device__ __forceinline__ void warp_bitonic_keys(KeyU32 (&v)[R], uint32_t lane) {
+#pragma unroll
+  for (int m = 1; m <= LEVELS; ++m) {
+    const int G = 1 << m;
+    {  // mirror stage
+      const bool lower = (lane & (G >> 1)) == 0;
+      uint32_t t[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) t[r] = __shfl_xor_sync(0xFFFFFFFFu, v[R - 1 - r].v, G - 1);
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r].v = lower ? min(v[r].v, t[r]) : max(v[r].v, t[r]);
+    }
+#pragma unroll
+    for (int dl = G >> 2; dl >= 1; dl >>= 1) {  // cross-lane half-cleaners
+      const bool lower = (lane & dl) == 0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const uint32_t p = __shfl_xor_sync(0xFFFFFFFFu, v[r].v, dl);
+        v[r].v = lower ? min(v[r].v, p) : max(v[r].v, p);
+      }
+    }
+#pragma unroll
+    for (int d = R >> 1; d >= 1; d >>= 1) {      // in-lane half-cleaners
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if ((r & d) == 0) KeyU32::cswap(v[r], v[r + d]);
+    }
+  }
+}
+
+// number of keys < x in the sorted run s[pad5(0 .. N)), N a power of two (branch-free)
+template <int N>
+__device__ __forceinline__ uint32_t lower_bound_keys(const uint32_t* s, uint32_t x) {
+  uint32_t p = 0;
+#pragma unroll
+  for (uint32_t st = N / 2; st >= 1; st >>= 1) p = s[pad<5>(p + st - 1)] < x ? p + st : p;
+  return p + (s[pad<5>(p)] < x ? 1u : 0u);
+}
+
+// Team sort of one block into sb (KElem32, key order): WP warps, warp `sub` holds the
+// elements e = sub*32*RS + lane + 32r.  sk: team scratch of WP*(32*RS + RS) words; cnt: team
+// scratch of WP*32*RS words.  Position k of sb gets the merge sentinel.
+template <int DT, int RS, int WP, int PS>
+__device__ __forceinline__ void team_sort_keys(KElem32* sb, const typename Traits<DT>::T (&raw)[RS], uint32_t k,
+                                               uint32_t sub, uint32_t lane, SyncTeam bar, uint32_t* sk,
+                                               uint32_t* cnt) {
+  constexpr int NS = 32 * RS;             // keys per warp
+  constexpr int SKW = NS + NS / 32;       // padded words per warp
+  const uint32_t tl = sub * 32 + lane;
+  {
+    uint4* c4 = reinterpret_cast<uint4*>(cnt);
+    for (uint32_t i = tl; i < (uint32_t)(WP * NS / 4); i += 32 * WP) c4[i] = make_uint4(0, 0, 0, 0);
+  }
+  uint32_t key[RS];
+  KeyU32 v[RS];
+#pragma unroll
+  for (int r = 0; r < RS; ++r) {
+    key[r] = Traits<DT>::enc(raw[r]);
+    v[r].v = key[r];
+  }
+  sort_regs<RS>(v);
+  warp_bitonic_keys<RS, 5>(v, lane);
+  uint32_t* mine = sk + sub * SKW;
+#pragma unroll
+  for (int r = 0; r < RS; ++r) mine[pad<5>((int)lane * RS + r)] = v[r].v;
+  if constexpr (WP > 1) bar(); else __syncwarp();
+#pragma unroll
+  for (int r = 0; r < RS; ++r) {
+    const uint32_t e = sub * NS + lane + 32 * r;
+    uint32_t pos = 0;
+#pragma unroll
+    for (int w = 0; w < WP; ++w) pos += lower_bound_keys<NS>(sk + w * SKW, key[r]);
+    if (e < k) {
+      pos += atomicAdd(&cnt[pos], 1u);
+      sb[pad<PS>((int)pos)] = KElem32::make(key[r], e);
+    }
+  }
+  if (tl == 0) sb[pad<PS>((int)k)] = KElem32::sentinel();
+  if constexpr (WP > 1) bar(); else __syncwarp();  // the scratch is reused by the next sort
+}
+
 template <typename TV, int RS, int WP>
 __device__ __forceinline__ void team_load_block(TV (&raw)[RS], const TV* x, uint64_t n, uint32_t k, uint64_t blk,
                                                 uint32_t sub, uint32_t lane) {

@@ -43,7 +43,12 @@ struct MediumCfg {
   using Tr = Traits<DT>;
   using U = typename Tr::U;
   // key-ordered elements: ties in any order (mf_sortnet.cuh)
-  using E = std::conditional_t<(R <= MF_MEDIUM_KEYORD_MAXR), typename KeyOrd<U>::E, Elem<U>>;
+#ifndef MF_KEYSORT
+#define MF_KEYSORT 1  // 32-bit keys: key-only network + rank recovery (team_sort_keys)
+#endif
+  // (R = 16: measured 2 % slower with it, the payload network is kept there)
+  static constexpr bool KS = MF_KEYSORT && sizeof(U) == 4 && R != 16;
+  using E = std::conditional_t<(KS || R <= MF_MEDIUM_KEYORD_MAXR), typename KeyOrd<U>::E, Elem<U>>;
   static constexpr int BS = 32 * R;        // block slot capacity (>= k)
   static constexpr int NW = 2 * R;         // words per merged row (2k bits <= 64R)
   static constexpr int RS = R / WP;        // elements per lane in the team block sort
@@ -60,7 +65,12 @@ struct MediumCfg {
   static constexpr int PS = pad_shift<RS>();
   static constexpr int SLOT = BS + (BS >> PS) + 1;
   static constexpr size_t sz_sorted = (sizeof(E) * SLOT * (W + 1) + 15) / 16 * 16;
-  static constexpr size_t sz_src = sizeof(uint16_t) * 2 * BS;  // merged pos -> (isB, sorted pos)
+  // merged pos -> key (MK), or -> (isB, sorted pos) where the keys would cost occupancy
+#ifndef MF_MK_MAXR
+#define MF_MK_MAXR 0  // largest R whose merged keys are stored (measured: the extra smem costs more occupancy than the saved load)
+#endif
+  static constexpr bool MK = R <= MF_MK_MAXR;
+  static constexpr size_t sz_src = (MK ? sizeof(U) : sizeof(uint16_t)) * 2 * BS;
   static constexpr size_t sz_rab = sizeof(uint32_t) * BS;      // RA | RB << 16, transposed [t][lane]
   static constexpr size_t sz_rows_bits = sizeof(uint32_t) * NW * CH;
   static constexpr size_t sz_stage = sizeof(U) * (BS + BS / 32 + 1);
@@ -80,8 +90,16 @@ __device__ __forceinline__ uint32_t row_addr(uint32_t L, uint32_t w) { return w 
 // sorts + a team merge level), runs the pair merge and the XOR prefix with 32*WP lanes,
 // and its first warp walks the 32 chunks.  WP = 2 for the largest blocks halves the
 // dependent merge chains that bound them at low occupancy.
+#ifndef MF_MINB_R8
+#define MF_MINB_R8 4  // resident CTAs the R = 8 kernel is compiled for (64-register cap: 1.19 -> 1.16 ms at k = 255)
+#endif
+#ifndef MF_MINB_R4
+#define MF_MINB_R4 0
+#endif
+template <int R> struct MediumMinBlocks { static constexpr int value = R == 8 ? MF_MINB_R8 : R == 4 ? MF_MINB_R4 : 0; };
+
 template <int DT, int R, int W, int WP>
-__global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t tiles_per_row, uint64_t total_tiles) {
+__global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_medium_kernel(Geom g, uint64_t tiles_per_row, uint64_t total_tiles) {
   using C = MediumCfg<DT, R, W, WP>;
   using Tr = typename C::Tr;
   using U = typename C::U;
@@ -112,6 +130,17 @@ __global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t
   TV pre[RS];                        // this lane's part of the team's next block, loaded during phase 2
   bool have_pre = false;
 
+  // sorted block into a ring slot; sorted position k holds a sentinel above every element,
+  // so the pair merge needs no bounds checks
+  auto sort_block = [&](E* sb, const TV (&raw)[RS]) {
+    if constexpr (C::KS) {
+      team_sort_keys<DT, RS, WP, PS>(sb, raw, k, sub, lane, tbar, rows, rab);
+    } else {
+      team_sort_raw<DT, RS, WP, C::BL>(sb, raw, k, sub, lane, tbar);
+      if (sub == 0 && lane == 0) sb[pad<PS>(k)] = E::sentinel();
+    }
+  };
+
   for (uint64_t t = t_begin; t < t_end; ++t) {
     const uint64_t row = t / tiles_per_row, tr = t % tiles_per_row;
     const uint64_t u0 = tr * W;
@@ -125,10 +154,10 @@ __global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t
     if (!carry && team == 0) {
       TV raw0[RS];
       team_load_block<TV, RS, WP>(raw0, x, g.n, k, u0, sub, lane);
-      team_sort_raw<DT, RS, WP, C::BL>(slot(0), raw0, k, sub, lane, tbar);
+      sort_block(slot(0), raw0);
     }
     if (!have_pre) team_load_block<TV, RS, WP>(pre, x, g.n, k, u0 + team + 1, sub, lane);
-    team_sort_raw<DT, RS, WP, C::BL>(slot(team + 1), pre, k, sub, lane, tbar);
+    sort_block(slot(team + 1), pre);
     __syncthreads();
     // prefetch this team's block of the next tile; it lands while phase 2 runs (large
     // blocks only: for small R the extra registers cost more occupancy than they hide)
@@ -163,39 +192,44 @@ __global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t
       const uint32_t w0 = (uint32_t)d >> 5, bo = (uint32_t)d & 31;
       uint32_t amask = 0;                        // A-side bits of this lane's positions (word w0)
       {
+        // merge path in the blocks' sort order, A before B on ties (E::merge_le); the
+        // search and the steps use the same order, so the lanes' ranges tile [0, 2k).
+        // Both blocks end in a sentinel at position k, so no step needs a bounds check.
         const int K = (int)k;
         int lo = d > K ? d - K : 0, hi = d < K ? d : K;
-        if (d >= (int)nq) lo = hi = 0;
         while (lo < hi) {
           const int mid = (lo + hi) >> 1;
-          if (A[pad<PS>(mid)].key() <= B[pad<PS>(d - 1 - mid)].key()) lo = mid + 1; else hi = mid;
+          if (E::merge_le(A[pad<PS>(mid)], B[pad<PS>(d - 1 - mid)])) lo = mid + 1; else hi = mid;
         }
-        int ia = lo, ib = d - lo;
-        E ea = A[pad<PS>(min(ia, K - 1))], eb = B[pad<PS>(min(max(ib, 0), K - 1))];
+        uint32_t ia = lo, ib = d - lo;
+        if (d >= (int)nq) ia = ib = K;             // lanes past the pair: both sides exhausted
+        E ea = A[pad<PS>(ia)], eb = B[pad<PS>(ib)];
         uint16_t* rab16 = reinterpret_cast<uint16_t*>(rab);
         uint32_t* rcol = rows + w0 * CH;         // row_addr<CH>(c, w0) = rcol[c ^ xr]
         const uint32_t xr = w0 & (CH - 1);
         constexpr int LSR = __builtin_ctz(SR);
 #pragma unroll 8
         for (int r = 0; r < PL; ++r) {
-          const int q = d + r;
-          const bool valid = q < (int)nq;
-          const bool takeA = (ib >= K) || (ia < K && ea.key() <= eb.key());
-          const uint32_t idx = sel(takeA, ea.idx(), eb.idx());
+          const uint32_t q = d + r;
+          const bool takeA = E::merge_le(ea, eb);
+          const E w = E::select(takeA, ea, eb);
+          // past the pair (q >= 2k) both sides are the sentinel: its index clamps to slot
+          // BS-1 >= k, whose rab entry and row bits beyond 2k nobody reads -- no branch
+          const uint32_t idx = min(w.idx(), (uint32_t)C::BS - 1);
           const uint32_t c = idx >> LSR;         // owning team lane (chunk) of this element
           const uint32_t bit = 1u << (bo + r);
-          if (valid) {
-            atomicOr(&rcol[c ^ xr], bit);
-            src[q] = (uint16_t)sel(takeA, (uint32_t)ia, 0x8000u | (uint32_t)ib);
-            rab16[2 * ((idx & (SR - 1)) * CH + c) + (takeA ? 0 : 1)] = (uint16_t)q;
-          }
-          amask |= (valid && takeA) ? bit : 0u;
+          atomicOr(&rcol[c ^ xr], bit);
+          if constexpr (C::MK) reinterpret_cast<U*>(src)[q] = w.key();
+          else src[q] = (uint16_t)sel(takeA, ia, 0x8000u | ib);
+          rab16[2 * ((idx & (SR - 1)) * CH + c) + (takeA ? 0 : 1)] = (uint16_t)q;
+          amask |= takeA ? bit : 0u;
           ia += takeA;
           ib += !takeA;
-          const E nv = (takeA ? A : B)[pad<PS>(min(sel(takeA, (uint32_t)ia, (uint32_t)ib), (uint32_t)K - 1))];
+          const E nv = (takeA ? A : B)[pad<PS>(min(sel(takeA, ia, ib), (uint32_t)K))];
           ea = E::select(takeA, nv, ea);
           eb = E::select(takeA, eb, nv);
         }
+        if (d + PL > (int)nq) amask &= d < (int)nq ? ((1u << (nq - d)) - 1u) << bo : 0u;
         if constexpr (!OWN)
           if (d < (int)nq) atomicOr(&abits[w0], amask);
       }
@@ -220,9 +254,13 @@ __global__ void __launch_bounds__(32 * W * WP) mf_medium_kernel(Geom g, uint64_t
 
       {
         auto key_at = [&](uint32_t p) -> U {
-          const uint32_t s = src[p];
-          const E* blk = (s & 0x8000u) ? B : A;   // one load from the selected block
-          return blk[pad<PS>(s & 0x7FFFu)].key();
+          if constexpr (C::MK) {
+            return reinterpret_cast<const U*>(src)[p];
+          } else {
+            const uint32_t s = src[p];
+            const E* blk = (s & 0x8000u) ? B : A;   // one load from the selected block
+            return blk[pad<PS>(s & 0x7FFFu)].key();
+          }
         };
 
         // walk: team lane L emits outputs [L*SR, L*SR + SR) of this unit

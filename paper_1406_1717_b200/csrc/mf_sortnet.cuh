@@ -54,6 +54,10 @@ template <> struct Elem<uint32_t> {
   __device__ __forceinline__ static Elem make(uint32_t key, uint32_t idx) {
     Elem e; e.v = ((uint64_t)key << 32) | idx; return e;
   }
+  // greater than every real or padding element in the full order
+  __device__ __forceinline__ static Elem sentinel() { Elem e; e.v = ~0ull; return e; }
+  // merge order of two sorted blocks (A before B on ties): the sort order itself
+  __device__ __forceinline__ static bool merge_le(const Elem& a, const Elem& b) { return a.v <= b.v; }
   __device__ __forceinline__ uint32_t key() const { return (uint32_t)(v >> 32); }
   __device__ __forceinline__ uint32_t idx() const { return (uint32_t)v; }
   __device__ __forceinline__ static bool less(const Elem& x, const Elem& y) { return x.v < y.v; }
@@ -75,6 +79,8 @@ template <> struct Elem<uint64_t> {
   __device__ __forceinline__ static Elem make(uint64_t key, uint32_t idx) {
     Elem e; e.k = key; e.i = idx; return e;
   }
+  __device__ __forceinline__ static Elem sentinel() { Elem e; e.k = ~0ull; e.i = ~0u; return e; }
+  __device__ __forceinline__ static bool merge_le(const Elem& a, const Elem& b) { return !less(b, a); }
   __device__ __forceinline__ uint64_t key() const { return k; }
   __device__ __forceinline__ uint32_t idx() const { return i; }
   __device__ __forceinline__ static bool less(const Elem& x, const Elem& y) {
@@ -105,6 +111,12 @@ struct KElem32 {
   __device__ __forceinline__ static KElem32 make(uint32_t key, uint32_t idx) {
     KElem32 e; e.v = ((uint64_t)key << 32) | idx; return e;
   }
+  __device__ __forceinline__ static KElem32 sentinel() { KElem32 e; e.v = ~0ull; return e; }
+  // merge order of two key-sorted blocks: by key, A first on ties, except that the
+  // sentinel (index bit 31) follows every real element of the same key
+  __device__ __forceinline__ static bool merge_le(const KElem32& a, const KElem32& b) {
+    return (a.v & 0xFFFFFFFF80000000ull) <= (b.v & 0xFFFFFFFF80000000ull);
+  }
   __device__ __forceinline__ uint32_t key() const { return (uint32_t)(v >> 32); }
   __device__ __forceinline__ uint32_t idx() const { return (uint32_t)v; }
   __device__ __forceinline__ static bool less(const KElem32& x, const KElem32& y) { return x.key() < y.key(); }
@@ -126,6 +138,10 @@ struct KElem64 {
   uint32_t i;
   __device__ __forceinline__ static KElem64 make(uint64_t key, uint32_t idx) {
     KElem64 e; e.k = key; e.i = idx; return e;
+  }
+  __device__ __forceinline__ static KElem64 sentinel() { KElem64 e; e.k = ~0ull; e.i = ~0u; return e; }
+  __device__ __forceinline__ static bool merge_le(const KElem64& a, const KElem64& b) {
+    return a.k < b.k || (a.k == b.k && (a.i >> 31) <= (b.i >> 31));
   }
   __device__ __forceinline__ uint64_t key() const { return k; }
   __device__ __forceinline__ uint32_t idx() const { return i; }
