@@ -240,34 +240,57 @@ __device__ __forceinline__ void warp_bitonic_keys(KeyU32 (&v)[R], uint32_t lane)
   }
 }
 
-// number of keys < x in the sorted run s[pad5(0 .. N)), N a power of two (branch-free)
+// number of keys < x in the sorted run s[pad5(0 .. N)), N a power of two (branch-free).
+// The search walks the padded index P = pad5(p) directly: at a step of size st the
+// position p is a multiple of 2*st, so the probe p + st - 1 sits at P + pad5(st - 1) (an
+// immediate load offset) and the step adds pad5(st) -- one compare and one predicated add
+// per step.  p is recovered at the end: P = 33a + b (b < 32) gives p = P - (P + 1) / 33.
+constexpr uint32_t cpad5(uint32_t q) { return q + (q >> 5); }
+// Plain (reorderable) shared load by shared-window address.  It is ordered after a barrier
+// only through its address: callers add order_token(), read after the barrier.
+__device__ __forceinline__ uint32_t lds32(uint32_t saddr) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr));
+  return v;
+}
+__device__ __forceinline__ uint32_t order_token() {
+  uint32_t z;
+  asm volatile("mov.u32 %0, 0;" : "=r"(z)::"memory");
+  return z;
+}
+
 template <int N>
-__device__ __forceinline__ uint32_t lower_bound_keys(const uint32_t* s, uint32_t x) {
-  uint32_t p = 0;
+__device__ __forceinline__ uint32_t lower_bound_keys(uint32_t s0, uint32_t x) {
+  uint32_t q = s0;  // s0: shared-window byte address of the run  // shared-window byte address of padded position P
 #pragma unroll
-  for (uint32_t st = N / 2; st >= 1; st >>= 1) p = s[pad<5>(p + st - 1)] < x ? p + st : p;
-  return p + (s[pad<5>(p)] < x ? 1u : 0u);
+  for (uint32_t st = N / 2; st >= 1; st >>= 1)
+    if (lds32(q + 4 * cpad5(st - 1)) < x) q += 4 * cpad5(st);
+  const uint32_t P = (q - s0) >> 2;
+  return P - (P + 1) / 33 + (lds32(q) < x ? 1u : 0u);
 }
 
 // the same count with 4-way steps: three independent loads per step, half the dependent chain
 template <int N>
-__device__ __forceinline__ uint32_t lower_bound_keys4(const uint32_t* s, uint32_t x) {
-  uint32_t p = 0;
+__device__ __forceinline__ uint32_t lower_bound_keys4(uint32_t s0, uint32_t x) {
+  uint32_t q = s0;
 #pragma unroll
   for (uint32_t st = N / 4; st >= 1; st >>= 2) {
-    const uint32_t c = (s[pad<5>(p + st - 1)] < x ? 1u : 0u) + (s[pad<5>(p + 2 * st - 1)] < x ? 1u : 0u) +
-                       (s[pad<5>(p + 3 * st - 1)] < x ? 1u : 0u);
-    p += c * st;
+    const uint32_t c = (lds32(q + 4 * cpad5(st - 1)) < x ? 1u : 0u) + (lds32(q + 4 * cpad5(2 * st - 1)) < x ? 1u : 0u) +
+                       (lds32(q + 4 * cpad5(3 * st - 1)) < x ? 1u : 0u);
+    const uint32_t a = c * st;
+    q += 4 * (st >= 16 ? a + (a >> 5) : a);
   }
-  if constexpr ((__builtin_ctz(N) & 1) != 0) p = s[pad<5>(p)] < x ? p + 1 : p;
-  return p + (s[pad<5>(p)] < x ? 1u : 0u);
+  if constexpr ((__builtin_ctz(N) & 1) != 0)
+    if (lds32(q) < x) q += 4;
+  const uint32_t P = (q - s0) >> 2;
+  return P - (P + 1) / 33 + (lds32(q) < x ? 1u : 0u);
 }
 
 #ifndef MF_LB4_MIN
 #define MF_LB4_MIN 1024  // smallest run searched with 4-way steps (measured: k = 1023 1.70 -> 1.64 ms, k = 255 +0.7 %)
 #endif
 template <int N>
-__device__ __forceinline__ uint32_t lower_bound_sel(const uint32_t* s, uint32_t x) {
+__device__ __forceinline__ uint32_t lower_bound_sel(uint32_t s, uint32_t x) {
   if constexpr (N >= MF_LB4_MIN) return lower_bound_keys4<N>(s, x);
   else return lower_bound_keys<N>(s, x);
 }
@@ -333,20 +356,29 @@ __device__ __forceinline__ void team_sort_keys(KElem32* sb, const typename Trait
     bar();
     srch = skm;
   }
+  // shared-window addresses of the sorted runs, tied to the barrier above
+  const uint32_t tok = order_token();
+  const uint32_t srch0 = (uint32_t)__cvta_generic_to_shared(srch) + tok;
+  uint32_t pos[RS];
+#pragma unroll
+  for (int r = 0; r < RS; ++r) {  // independent searches (no branch: they interleave)
+    pos[r] = 0;
+    if constexpr (MERGE) {
+      pos[r] = lower_bound_sel<2 * NS>(srch0, key[r]);
+    } else {
+#pragma unroll
+      for (int w = 0; w < WP; ++w) pos[r] += lower_bound_sel<NS>(srch0 + 4 * w * SKW, key[r]);
+    }
+  }
+  // tie slots and the scatter, branch-free: slot fillers count on cnt[BS-1] (never a real
+  // element's rank, which is < k <= BS-1) and write the unused slot position BS
+  constexpr uint32_t BS = WP * NS;
 #pragma unroll
   for (int r = 0; r < RS; ++r) {
     const uint32_t e = sub * NS + lane + 32 * r;
-    uint32_t pos = 0;
-    if constexpr (MERGE) {
-      pos = lower_bound_sel<2 * NS>(srch, key[r]);
-    } else {
-#pragma unroll
-      for (int w = 0; w < WP; ++w) pos += lower_bound_sel<NS>(sk + w * SKW, key[r]);
-    }
-    if (e < k) {
-      pos += atomicAdd(&cnt[pos], 1u);
-      sb[pad<PS>((int)pos)] = KElem32::make(key[r], e);
-    }
+    const bool real = e < k;
+    const uint32_t t = atomicAdd(&cnt[real ? pos[r] : BS - 1], 1u);
+    sb[pad<PS>((int)(real ? pos[r] + t : BS))] = KElem32::make(key[r], e);
   }
   if (tl == 0) sb[pad<PS>((int)k)] = KElem32::sentinel();
   if constexpr (WP > 1) bar(); else __syncwarp();  // the scratch is reused by the next sort
