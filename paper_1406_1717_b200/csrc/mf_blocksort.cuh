@@ -301,7 +301,11 @@ __device__ __forceinline__ uint32_t lower_bound_sel(uint32_t s, uint32_t x) {
 // Team sort of one block into sb (KElem32, key order): WP warps, warp `sub` holds the
 // elements e = sub*32*RS + lane + 32r.  sk: team scratch of 2*WP*(32*RS + RS) words; cnt: team
 // scratch of WP*32*RS words.  Position k of sb gets the merge sentinel.
-template <int DT, int RS, int WP, int PS>
+// The element's index is stored as ridx = (e % SRr) * CHr + e / SRr (the walk's transposed
+// [step][chunk] slot of e; SRr = 0 stores e itself).  The sentinel's low word is 0xFFFFFFFF
+// when a real element of the block has the all-ones key (it would tie with the sentinel),
+// else 0xFFFFFFFE; both have bit 31 set (KElem32::merge_le).
+template <int DT, int RS, int WP, int PS, int SRr = 0, int CHr = 1>
 __device__ __forceinline__ void team_sort_keys(KElem32* sb, const typename Traits<DT>::T (&raw)[RS], uint32_t k,
                                                uint32_t sub, uint32_t lane, SyncTeam bar, uint32_t* sk,
                                                uint32_t* cnt) {
@@ -373,15 +377,24 @@ __device__ __forceinline__ void team_sort_keys(KElem32* sb, const typename Trait
   // tie slots and the scatter, branch-free: slot fillers count on cnt[BS-1] (never a real
   // element's rank, which is < k <= BS-1) and write the unused slot position BS
   constexpr uint32_t BS = WP * NS;
+  bool maxkey = false;
 #pragma unroll
   for (int r = 0; r < RS; ++r) {
     const uint32_t e = sub * NS + lane + 32 * r;
     const bool real = e < k;
+    maxkey |= real && key[r] == 0xFFFFFFFFu;
     const uint32_t t = atomicAdd(&cnt[real ? pos[r] : BS - 1], 1u);
-    sb[pad<PS>((int)(real ? pos[r] + t : BS))] = KElem32::make(key[r], e);
+    uint32_t ri = e;
+    if constexpr (SRr > 0) ri = (e & (SRr - 1)) * CHr + e / SRr;
+    sb[pad<PS>((int)(real ? pos[r] + t : BS))] = KElem32::make(key[r], ri);
   }
-  if (tl == 0) sb[pad<PS>((int)k)] = KElem32::sentinel();
-  if constexpr (WP > 1) bar(); else __syncwarp();  // the scratch is reused by the next sort
+  // the scratch is reused by the next sort
+  if constexpr (WP > 1) maxkey = bar.any(maxkey); else maxkey = __any_sync(0xFFFFFFFFu, maxkey);
+  if (tl == 0) {
+    KElem32 s = KElem32::sentinel();
+    if (!maxkey) s.v &= ~1ull;
+    sb[pad<PS>((int)k)] = s;
+  }
 }
 
 template <typename TV, int RS, int WP>

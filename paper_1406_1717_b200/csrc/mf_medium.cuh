@@ -61,8 +61,9 @@ struct MediumCfg {
 #define MF_BL_WARP 5  // ... in 1-warp teams (5: the whole block in registers)
 #endif
   static constexpr int BL = WP > 1 ? MF_BL_TEAM : MF_BL_WARP;
-  // padded element index: blocked per-lane writes hit distinct banks (8-byte elements)
-  static constexpr int PS = pad_shift<RS>();
+  // padded element index: blocked per-lane writes hit distinct banks (8-byte elements);
+  // the key sort scatters, so its slots are unpadded (the merge walks byte addresses)
+  static constexpr int PS = KS ? 30 : pad_shift<RS>();
   static constexpr int SLOT = BS + (BS >> PS) + 1;
   static constexpr size_t sz_sorted = (sizeof(E) * SLOT * (W + 1) + 15) / 16 * 16;
   // merged pos -> key (MK), or -> (isB, sorted pos) where the keys would cost occupancy
@@ -134,11 +135,78 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
   // so the pair merge needs no bounds checks
   auto sort_block = [&](E* sb, const TV (&raw)[RS]) {
     if constexpr (C::KS) {
-      team_sort_keys<DT, RS, WP, PS>(sb, raw, k, sub, lane, tbar, rows, rab);
+      team_sort_keys<DT, RS, WP, PS, SR, CH>(sb, raw, k, sub, lane, tbar, rows, rab);
     } else {
       team_sort_raw<DT, RS, WP, C::BL>(sb, raw, k, sub, lane, tbar);
       if (sub == 0 && lane == 0) sb[pad<PS>(k)] = E::sentinel();
     }
+  };
+
+  // Pair merge of the key-sorted slots A, B (KS): team lane owns merged positions
+  // [d, d + PL).  The cursors are shared-window byte addresses; elements carry ridx (the
+  // transposed rab slot of their index, team_sort_keys), so the chunk is ridx % CH and the
+  // rab entry 2*ridx + side.  Unless B holds a real all-ones key (its sentinel's bit 0),
+  // plain key compares order the pair: A's sentinel then never ties with a live B element.
+  // src[q] gets the byte offset of the key of merged position q.  Returns the A bits.
+  auto merge_keys = [&](const auto* A, const auto* B, int d, uint32_t w0, uint32_t bo) -> uint32_t {
+    constexpr int PL = 2 * R / WP;
+    const uint32_t ringS = (uint32_t)__cvta_generic_to_shared(ring) + order_token();
+    const uint32_t offA = (uint32_t)(reinterpret_cast<const unsigned char*>(A) - reinterpret_cast<const unsigned char*>(ring));
+    const uint32_t offB = (uint32_t)(reinterpret_cast<const unsigned char*>(B) - reinterpret_cast<const unsigned char*>(ring));
+    const int K = (int)k;
+    const bool exact = (B[K].v & 1ull) != 0;
+    uint16_t* rab16 = reinterpret_cast<uint16_t*>(rab);
+    uint32_t* rcol = rows + w0 * CH;
+    const uint32_t xr = w0 & (CH - 1);
+    auto run = [&](auto ex) -> uint32_t {
+      constexpr bool EX = decltype(ex)::value;
+      auto le = [&](uint2 a, uint2 b) -> bool {
+        if constexpr (EX) {
+          return (((uint64_t)a.y << 32) | (a.x & 0x80000000u)) <= (((uint64_t)b.y << 32) | (b.x & 0x80000000u));
+        } else {
+          return a.y <= b.y;
+        }
+      };
+      auto at = [&](uint32_t off) -> uint2 {
+        uint2 v;
+        asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(ringS + off));
+        return v;
+      };
+      int lo = d > K ? d - K : 0, hi = d < K ? d : K;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (le(at(offA + 8 * mid), at(offB + 8 * (d - 1 - mid)))) lo = mid + 1; else hi = mid;
+      }
+      uint32_t ia = lo, ib = d - lo;
+      if (d >= (int)nq) ia = ib = K;             // lanes past the pair: both sides exhausted
+      uint32_t relA = offA + 8 * ia, relB = offB + 8 * ib;
+      const uint32_t limA = offA + 8 * K;
+      uint2 ea = at(relA), eb = at(relB);
+      uint32_t bit = 1u << bo, am = 0;
+#pragma unroll 8
+      for (int r = 0; r < PL; ++r) {
+        const uint32_t q = d + r;
+        const bool takeA = le(ea, eb);
+        // past the pair both sides are the sentinel: ridx clamps to BS-1 >= k, whose rab
+        // entry and row bits beyond 2k nobody reads -- no branch
+        const uint32_t ri = min(takeA ? ea.x : eb.x, (uint32_t)C::BS - 1);
+        atomicOr(&rcol[(ri & (CH - 1)) ^ xr], bit);
+        src[q] = (uint16_t)((takeA ? relA : relB) + 4);
+        rab16[2 * ri + (takeA ? 0 : 1)] = (uint16_t)q;
+        am |= takeA ? bit : 0u;
+        bit <<= 1;
+        relA += takeA ? 8u : 0u;
+        relB += takeA ? 0u : 8u;
+        // only A can pass its sentinel (ties go to A); B never passes it
+        const uint2 nv = at(takeA ? min(relA, limA) : relB);
+        ea = takeA ? nv : ea;
+        eb = takeA ? eb : nv;
+      }
+      return am;
+    };
+    uint32_t am = exact ? run(std::true_type{}) : run(std::false_type{});
+    if (d + PL > (int)nq) am &= d < (int)nq ? ((1u << (nq - d)) - 1u) << bo : 0u;
+    return am;
   };
 
   for (uint64_t t = t_begin; t < t_end; ++t) {
@@ -191,7 +259,9 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
       const int d = tl * PL;
       const uint32_t w0 = (uint32_t)d >> 5, bo = (uint32_t)d & 31;
       uint32_t amask = 0;                        // A-side bits of this lane's positions (word w0)
-      {
+      if constexpr (C::KS) {
+        amask = merge_keys(A, B, d, w0, bo);
+      } else {
         // merge path in the blocks' sort order, A before B on ties (E::merge_le); the
         // search and the steps use the same order, so the lanes' ranges tile [0, 2k).
         // Both blocks end in a sentinel at position k, so no step needs a bounds check.
@@ -230,9 +300,9 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
           eb = E::select(takeA, eb, nv);
         }
         if (d + PL > (int)nq) amask &= d < (int)nq ? ((1u << (nq - d)) - 1u) << bo : 0u;
-        if constexpr (!OWN)
-          if (d < (int)nq) atomicOr(&abits[w0], amask);
       }
+      if constexpr (!OWN)
+        if (d < (int)nq) atomicOr(&abits[w0], amask);
       // XOR prefix over chunks: row_L = A_bits ^ (toggles of chunks < L).  A lane that owns
       // its word wrote every toggle of it itself, so it needs no barrier before its prefix.
       auto prefix = [&](uint32_t w, uint32_t acc) {
@@ -253,8 +323,13 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
       team_sync();
 
       {
+        const uint32_t ringK = (uint32_t)__cvta_generic_to_shared(ring);
         auto key_at = [&](uint32_t p) -> U {
-          if constexpr (C::MK) {
+          if constexpr (C::KS) {
+            uint32_t v;
+            asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(ringK + src[p]));
+            return (U)v;
+          } else if constexpr (C::MK) {
             return reinterpret_cast<const U*>(src)[p];
           } else {
             const uint32_t s = src[p];
