@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_
   using U = typename C::U;
   using TV = typename Tr::T;
 #ifndef MF_SMALL_KEYORD_MAXK
-#define MF_SMALL_KEYORD_MAXK 15  // (measured: k = 3..15 4-8 % faster, k = 31 16 % slower)
+#define MF_SMALL_KEYORD_MAXK 31  // (measured: k = 3..15 4-8 %, k = 23..31 8-12 % faster)
 #endif
   // key-ordered elements (one compare per exchange): equal keys may take either order
   // inside a block, which changes no emitted median

@@ -105,6 +105,9 @@ template <> struct Elem<uint64_t> {
 // exchange.  Decisions taken separately by two lanes about the same pair (bitonic
 // cross-lane stages) use less_full, so both lanes agree on ties.  Phase-API sorts, whose
 // permutation must match piecewise_sort (filter.hpp:41-54), keep Elem.
+#ifndef MF_KE_PLAIN
+#define MF_KE_PLAIN 1  // plain selects let ptxas schedule the network (measured: k = 31 small kernel 0.50 -> 0.46 ms)
+#endif
 struct KElem32 {
   static constexpr bool kFull = false;  // ordered by key only
   uint64_t v;  // key << 32 | index
@@ -124,8 +127,13 @@ struct KElem32 {
   __device__ __forceinline__ static void cswap(KElem32& x, KElem32& y) {
     const bool sw = y.key() < x.key();
     const uint64_t a = x.v, b = y.v;
+#if MF_KE_PLAIN
+    x.v = sw ? b : a;
+    y.v = sw ? a : b;
+#else
     x.v = sel(sw, b, a);
     y.v = sel(sw, a, b);
+#endif
   }
   __device__ __forceinline__ static KElem32 select(bool c, const KElem32& a, const KElem32& b) {
     KElem32 e; e.v = sel(c, a.v, b.v); return e;
