@@ -74,6 +74,13 @@ struct Geom {
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
 // Forced select (selp): both operands are computed, so no divergent branch is emitted.
+#ifndef MF_SEL_PLAIN
+#define MF_SEL_PLAIN 1  // plain ternaries: ptxas still emits selects, and schedules them better (k = 31 -3 %)
+#endif
+#if MF_SEL_PLAIN
+__device__ __forceinline__ uint32_t sel(bool c, uint32_t a, uint32_t b) { return c ? a : b; }
+__device__ __forceinline__ uint64_t sel(bool c, uint64_t a, uint64_t b) { return c ? a : b; }
+#else
 __device__ __forceinline__ uint32_t sel(bool c, uint32_t a, uint32_t b) {
   uint32_t r;
   asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\tselp.b32 %0, %2, %3, p;\n\t}"
@@ -86,6 +93,7 @@ __device__ __forceinline__ uint64_t sel(bool c, uint64_t a, uint64_t b) {
       : "=l"(r) : "r"((uint32_t)c), "l"(a), "l"(b));
   return r;
 }
+#endif
 
 
 }  // namespace mf

@@ -95,9 +95,24 @@ __device__ __forceinline__ uint32_t row_addr(uint32_t L, uint32_t w) { return w 
 #define MF_MINB_R8 4  // resident CTAs the R = 8 kernel is compiled for (64-register cap: 1.19 -> 1.16 ms at k = 255)
 #endif
 #ifndef MF_MINB_R4
-#define MF_MINB_R4 0
+#define MF_MINB_R4 4  // (64 registers: k = 101 1.65 -> 1.45 ms)
 #endif
 template <int R> struct MediumMinBlocks { static constexpr int value = R == 8 ? MF_MINB_R8 : R == 4 ? MF_MINB_R4 : 0; };
+
+// src[] holds one entry per merged position q, stored [q % PL][q / PL] (PL = positions per
+// team lane): the merge's per-lane runs of PL positions then store conflict-free.
+template <int PL, int TL>
+__device__ __forceinline__ uint32_t src_slot(uint32_t q) {
+  return (q & (PL - 1)) * TL + (q >> __builtin_ctz(PL));
+}
+
+#ifndef MF_MERGE_NC32
+#define MF_MERGE_NC32 1  // independent pair-merge chains per lane for R = 32 (measured: 2 is 7 % slower)
+#endif
+#ifndef MF_MERGE_NC8
+#define MF_MERGE_NC8 1
+#endif
+template <int R> struct MergeChains { static constexpr int value = R == 32 ? MF_MERGE_NC32 : R == 8 ? MF_MERGE_NC8 : 1; };
 
 template <int DT, int R, int W, int WP>
 __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_medium_kernel(Geom g, uint64_t tiles_per_row, uint64_t total_tiles) {
@@ -172,35 +187,63 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
         asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(ringS + off));
         return v;
       };
-      int lo = d > K ? d - K : 0, hi = d < K ? d : K;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (le(at(offA + 8 * mid), at(offB + 8 * (d - 1 - mid)))) lo = mid + 1; else hi = mid;
+      // NC independent merge chains per lane (sub-ranges of PLC positions), interleaved
+      // step by step: the dependent shared-load chain of each is NC times shorter
+      constexpr int NC = MergeChains<R>::value, PLC = PL / NC;
+      uint32_t lo[NC], hi[NC];
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        const uint32_t dj = d + j * PLC;
+        lo[j] = dj > (uint32_t)K ? dj - K : 0;
+        hi[j] = dj < (uint32_t)K ? dj : K;
       }
-      uint32_t ia = lo, ib = d - lo;
-      if (d >= (int)nq) ia = ib = K;             // lanes past the pair: both sides exhausted
-      uint32_t relA = offA + 8 * ia, relB = offB + 8 * ib;
+      const int niter = 32 - __clz(K);          // >= ceil(log2(K + 1)) halvings
+      for (int it = 0; it < niter; ++it) {
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          const uint32_t dj = d + j * PLC;
+          const bool act = lo[j] < hi[j];
+          const uint32_t mid = (lo[j] + hi[j]) >> 1;
+          const bool g = le(at(offA + 8 * (act ? mid : 0u)), at(offB + 8 * (act ? dj - 1 - mid : 0u)));
+          lo[j] = act && g ? mid + 1 : lo[j];
+          hi[j] = act && !g ? mid : hi[j];
+        }
+      }
       const uint32_t limA = offA + 8 * K;
-      uint2 ea = at(relA), eb = at(relB);
-      uint32_t bit = 1u << bo, am = 0;
+      uint32_t relA[NC], relB[NC], bit[NC], am = 0;
+      uint2 ea[NC], eb[NC];
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        const uint32_t dj = d + j * PLC;
+        uint32_t ia = lo[j], ib = dj - lo[j];
+        if (dj >= nq) ia = ib = K;               // chains past the pair: both sides exhausted
+        relA[j] = offA + 8 * ia;
+        relB[j] = offB + 8 * ib;
+        ea[j] = at(relA[j]);
+        eb[j] = at(relB[j]);
+        bit[j] = 1u << (bo + j * PLC);
+      }
 #pragma unroll 8
-      for (int r = 0; r < PL; ++r) {
-        const uint32_t q = d + r;
-        const bool takeA = le(ea, eb);
-        // past the pair both sides are the sentinel: ridx clamps to BS-1 >= k, whose rab
-        // entry and row bits beyond 2k nobody reads -- no branch
-        const uint32_t ri = min(takeA ? ea.x : eb.x, (uint32_t)C::BS - 1);
-        atomicOr(&rcol[(ri & (CH - 1)) ^ xr], bit);
-        src[q] = (uint16_t)((takeA ? relA : relB) + 4);
-        rab16[2 * ri + (takeA ? 0 : 1)] = (uint16_t)q;
-        am |= takeA ? bit : 0u;
-        bit <<= 1;
-        relA += takeA ? 8u : 0u;
-        relB += takeA ? 0u : 8u;
-        // only A can pass its sentinel (ties go to A); B never passes it
-        const uint2 nv = at(takeA ? min(relA, limA) : relB);
-        ea = takeA ? nv : ea;
-        eb = takeA ? eb : nv;
+      for (int r = 0; r < PLC; ++r) {
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          const uint32_t q = d + j * PLC + r;
+          const bool takeA = le(ea[j], eb[j]);
+          // past the pair both sides are the sentinel: ridx clamps to BS-1 >= k, whose rab
+          // entry and row bits beyond 2k nobody reads -- no branch
+          const uint32_t ri = min(takeA ? ea[j].x : eb[j].x, (uint32_t)C::BS - 1);
+          atomicOr(&rcol[(ri & (CH - 1)) ^ xr], bit[j]);
+          src[src_slot<PL, 32 * WP>(q)] = (uint16_t)((takeA ? relA[j] : relB[j]) + 4);
+          rab16[2 * ri + (takeA ? 0 : 1)] = (uint16_t)q;
+          am |= takeA ? bit[j] : 0u;
+          bit[j] <<= 1;
+          relA[j] += takeA ? 8u : 0u;
+          relB[j] += takeA ? 0u : 8u;
+          // only A can pass its sentinel (ties go to A); B never passes it
+          const uint2 nv = at(takeA ? min(relA[j], limA) : relB[j]);
+          ea[j] = takeA ? nv : ea[j];
+          eb[j] = takeA ? eb[j] : nv;
+        }
       }
       return am;
     };
@@ -290,7 +333,7 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
           const uint32_t bit = 1u << (bo + r);
           atomicOr(&rcol[c ^ xr], bit);
           if constexpr (C::MK) reinterpret_cast<U*>(src)[q] = w.key();
-          else src[q] = (uint16_t)sel(takeA, ia, 0x8000u | ib);
+          else src[src_slot<PL, TL>(q)] = (uint16_t)sel(takeA, ia, 0x8000u | ib);
           rab16[2 * ((idx & (SR - 1)) * CH + c) + (takeA ? 0 : 1)] = (uint16_t)q;
           amask |= takeA ? bit : 0u;
           ia += takeA;
@@ -327,12 +370,12 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
         auto key_at = [&](uint32_t p) -> U {
           if constexpr (C::KS) {
             uint32_t v;
-            asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(ringK + src[p]));
+            asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(ringK + src[src_slot<PL, TL>(p)]));
             return (U)v;
           } else if constexpr (C::MK) {
             return reinterpret_cast<const U*>(src)[p];
           } else {
-            const uint32_t s = src[p];
+            const uint32_t s = src[src_slot<PL, TL>(p)];
             const E* blk = (s & 0x8000u) ? B : A;   // one load from the selected block
             return blk[pad<PS>(s & 0x7FFFu)].key();
           }
