@@ -38,6 +38,10 @@ namespace mf {
 #define MF_MEDIUM_KEYORD_MAXR 16  // largest R sorted with key-ordered elements (R = 32: measured slower)
 #endif
 
+#ifndef MF_ROWS_PAD
+#define MF_ROWS_PAD 1
+#endif
+
 template <int DT, int R, int W, int WP = 1>
 struct MediumCfg {
   using Tr = Traits<DT>;
@@ -73,19 +77,25 @@ struct MediumCfg {
   static constexpr bool MK = R <= MF_MK_MAXR;
   static constexpr size_t sz_src = (MK ? sizeof(U) : sizeof(uint16_t)) * 2 * BS;
   static constexpr size_t sz_rab = sizeof(uint32_t) * BS;      // RA | RB << 16, transposed [t][lane]
-  static constexpr size_t sz_rows_bits = sizeof(uint32_t) * NW * CH;
+  static constexpr int NWP = MF_ROWS_PAD ? NW + 1 : NW;  // row stride in words (rows[L][w] at L*NWP + w)
+  static constexpr size_t sz_rows_bits = sizeof(uint32_t) * NWP * CH;
   static constexpr size_t sz_stage = sizeof(U) * (BS + BS / 32 + 1);
   // the rows area doubles as the output staging area after the walk
-  static constexpr size_t sz_rows = (sz_rows_bits > sz_stage ? sz_rows_bits : sz_stage + 15) / 16 * 16;
+  static constexpr size_t sz_rows = ((sz_rows_bits > sz_stage ? sz_rows_bits : sz_stage) + 15) / 16 * 16;
   static constexpr size_t sz_abits = sizeof(uint32_t) * NW;
   static constexpr size_t sz_warp = (sz_src + sz_rab + sz_rows + sz_abits + 15) / 16 * 16;  // per team
   static constexpr size_t smem = sz_sorted + W * sz_warp;
 };
 
-// rows[L][w] lives at w*32 + (L ^ (w & 31)): the prefix pass (lane = word, loop
-// over L) and the walk (lane = L, data-dependent word) are both bank-spread.
-template <int CH>
-__device__ __forceinline__ uint32_t row_addr(uint32_t L, uint32_t w) { return w * CH + (L ^ (w & (CH - 1))); }
+// Row L of the per-chunk live sets, word w.  Padded layout (MF_ROWS_PAD): rows[L][w] at
+// L*NWP + w with an odd stride NWP, so the prefix pass (lane = word, loop over L: immediate
+// offsets) and the walk (lane = L, data-dependent word) are both bank-spread.  Otherwise
+// rows[L][w] at w*CH + (L ^ (w & (CH-1))).
+template <int CH, int NWP>
+__device__ __forceinline__ uint32_t row_addr(uint32_t L, uint32_t w) {
+  if constexpr (MF_ROWS_PAD) return L * NWP + w;
+  else return w * CH + (L ^ (w & (CH - 1)));
+}
 
 // A "team" of WP warps owns one block pair: it sorts the pair's B block together (WP warp
 // sorts + a team merge level), runs the pair merge and the XOR prefix with 32*WP lanes,
@@ -171,8 +181,6 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
     const int K = (int)k;
     const bool exact = (B[K].v & 1ull) != 0;
     uint16_t* rab16 = reinterpret_cast<uint16_t*>(rab);
-    uint32_t* rcol = rows + w0 * CH;
-    const uint32_t xr = w0 & (CH - 1);
     auto run = [&](auto ex) -> uint32_t {
       constexpr bool EX = decltype(ex)::value;
       auto le = [&](uint2 a, uint2 b) -> bool {
@@ -232,7 +240,7 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
           // past the pair both sides are the sentinel: ridx clamps to BS-1 >= k, whose rab
           // entry and row bits beyond 2k nobody reads -- no branch
           const uint32_t ri = min(takeA ? ea[j].x : eb[j].x, (uint32_t)C::BS - 1);
-          atomicOr(&rcol[(ri & (CH - 1)) ^ xr], bit[j]);
+          atomicOr(&rows[row_addr<CH, C::NWP>(ri & (CH - 1), w0)], bit[j]);
           src[src_slot<PL, 32 * WP>(q)] = (uint16_t)((takeA ? relA[j] : relB[j]) + 4);
           rab16[2 * ri + (takeA ? 0 : 1)] = (uint16_t)q;
           am |= takeA ? bit[j] : 0u;
@@ -291,7 +299,7 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
       constexpr bool OWN = PL == 32;             // each lane owns one whole word of every row
       {
         uint4* r4 = reinterpret_cast<uint4*>(rows);
-        for (uint32_t i = tl; i < NW * CH / 4; i += TL) r4[i] = make_uint4(0, 0, 0, 0);
+        for (uint32_t i = tl; i < (C::NWP * CH + 3) / 4; i += TL) r4[i] = make_uint4(0, 0, 0, 0);
         if constexpr (!OWN)
           for (uint32_t w = tl; w < NW; w += TL) abits[w] = 0;
       }
@@ -318,8 +326,6 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
         if (d >= (int)nq) ia = ib = K;             // lanes past the pair: both sides exhausted
         E ea = A[pad<PS>(ia)], eb = B[pad<PS>(ib)];
         uint16_t* rab16 = reinterpret_cast<uint16_t*>(rab);
-        uint32_t* rcol = rows + w0 * CH;         // row_addr<CH>(c, w0) = rcol[c ^ xr]
-        const uint32_t xr = w0 & (CH - 1);
         constexpr int LSR = __builtin_ctz(SR);
 #pragma unroll 8
         for (int r = 0; r < PL; ++r) {
@@ -331,7 +337,7 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
           const uint32_t idx = min(w.idx(), (uint32_t)C::BS - 1);
           const uint32_t c = idx >> LSR;         // owning team lane (chunk) of this element
           const uint32_t bit = 1u << (bo + r);
-          atomicOr(&rcol[c ^ xr], bit);
+          atomicOr(&rows[row_addr<CH, C::NWP>(c, w0)], bit);
           if constexpr (C::MK) reinterpret_cast<U*>(src)[q] = w.key();
           else src[src_slot<PL, TL>(q)] = (uint16_t)sel(takeA, ia, 0x8000u | ib);
           rab16[2 * ((idx & (SR - 1)) * CH + c) + (takeA ? 0 : 1)] = (uint16_t)q;
@@ -351,7 +357,7 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
       auto prefix = [&](uint32_t w, uint32_t acc) {
 #pragma unroll 8
         for (uint32_t L = 0; L < (uint32_t)CH; ++L) {
-          const uint32_t a = row_addr<CH>(L, w);
+          const uint32_t a = row_addr<CH, C::NWP>(L, w);
           const uint32_t dlt = rows[a];
           rows[a] = acc;
           acc ^= dlt;
@@ -392,7 +398,7 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
             uint32_t wv[G], pc[G], sg = 0;
 #pragma unroll
             for (int j = 0; j < G; ++j) {
-              wv[j] = rows[row_addr<CH>(tl, G > 1 ? min(cw + j, nw - 1) : cw)];
+              wv[j] = rows[row_addr<CH, C::NWP>(tl, G > 1 ? min(cw + j, nw - 1) : cw)];
               pc[j] = (G == 1 || cw + j < nw) ? __popc(wv[j]) : 0u;
               sg += pc[j];
             }
@@ -420,8 +426,8 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
               const uint32_t ba = 1u << (a & 31), bb = 1u << (b & 31);
               // Delete(A, i-1) and Undelete(B, i-1), written through to the row in shared
               // memory (fire-and-forget atomics, no divergence) and to the cached cursor word
-              atomicAnd(&rows[row_addr<CH>(tl, a >> 5)], ~ba);
-              atomicOr(&rows[row_addr<CH>(tl, b >> 5)], bb);
+              atomicAnd(&rows[row_addr<CH, C::NWP>(tl, a >> 5)], ~ba);
+              atomicOr(&rows[row_addr<CH, C::NWP>(tl, b >> 5)], bb);
               cb = sel((a >> 5) == cw, cb & ~ba, cb);
               cb = sel((b >> 5) == cw, cb | bb, cb);
               // the cursor moves up when the deletion is at or below it and the insertion above
@@ -433,7 +439,7 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
               uint32_t m = sel(up, mu, md);
               if ((up || down) && m == 0) {  // the next live position is in another word (rare)
                 const int dir = up ? 1 : -1;
-                do { cw += dir; cb = rows[row_addr<CH>(tl, cw)]; m = cb; } while (m == 0);
+                do { cw += dir; cb = rows[row_addr<CH, C::NWP>(tl, cw)]; m = cb; } while (m == 0);
               }
               p = sel(up, cw * 32 + __ffs(m) - 1, sel(down, cw * 32 + 31 - __clz(m), p));
               out[t] = key_at(p);
