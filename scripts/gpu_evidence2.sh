@@ -8,6 +8,6 @@ python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ev_plain.log
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum --clock-control none --csv \
     --log-file gpurun_out/ev_launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ev_ncu1.log 2>&1
 python scripts/profile_c2.py > gpurun_out/ev_plain2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:mf_ -s 1 -c 8 -o gpurun_out/ev_full -f \
-    python scripts/profile_c2.py 3 3 31 31 255 255 1023 1023 > gpurun_out/ev_ncu2.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:mf_ -s 0 -c 8 -o gpurun_out/ev_full -f \
+    python scripts/profile_c2.py 3 31 255 1023 > gpurun_out/ev_ncu2.log 2>&1
 tail -2 gpurun_out/ev_ncu2.log
