@@ -26,7 +26,7 @@ struct mf_context {
   uint64_t launches = 0;
   // host-entry pipeline: H2D / compute / D2H on three streams, up to 4 chunks in flight
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
-  cudaEvent_t ev_in[4] = {}, ev_done[4] = {}, ev_out[4] = {};
+  cudaEvent_t ev_in[16] = {}, ev_done[16] = {}, ev_out[16] = {};
   std::mutex mu;
 };
 
@@ -176,7 +176,7 @@ void mf_context_destroy(mf_context* ctx) {
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->s_h2d) cudaStreamSynchronize(ctx->s_h2d), cudaStreamDestroy(ctx->s_h2d);
   if (ctx->s_d2h) cudaStreamSynchronize(ctx->s_d2h), cudaStreamDestroy(ctx->s_d2h);
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 16; ++i) {
     if (ctx->ev_in[i]) cudaEventDestroy(ctx->ev_in[i]);
     if (ctx->ev_done[i]) cudaEventDestroy(ctx->ev_done[i]);
     if (ctx->ev_out[i]) cudaEventDestroy(ctx->ev_out[i]);
@@ -256,7 +256,13 @@ mf_status mf_median_filter_rows(mf_context* ctx, mf_dtype dtype, const void* x, 
   if (keep == 0 || rows == 0) return MF_OK;
   if (!x || !y || ld_x < n || ld_y < keep) return MF_BAD_ARG;
   if (cudaSetDevice(ctx->device) != cudaSuccess) return MF_NO_DEVICE;
-  constexpr int kNumSlots = 4;
+#ifndef MF_PIPE_SLOTS
+#define MF_PIPE_SLOTS 4
+#endif
+#ifndef MF_PIPE_RAMP
+#define MF_PIPE_RAMP 16
+#endif
+  constexpr int kNumSlots = MF_PIPE_SLOTS;
   const size_t kChunkElems = ctx->chunk_elems;
   if (!ctx->s_h2d) {
     if (cudaStreamCreateWithFlags(&ctx->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
@@ -275,7 +281,7 @@ mf_status mf_median_filter_rows(mf_context* ctx, mf_dtype dtype, const void* x, 
   const bool by_rows = rows > 1;
   const size_t total = by_rows ? rows : keep;                                               // units to cut
   const size_t cmax = by_rows ? std::max<size_t>(1, kChunkElems / n) : std::min(keep, std::max<size_t>(kChunkElems, 16 * k));
-  const size_t cmin = std::max<size_t>(by_rows ? 1 : std::min(cmax, 16 * k), cmax / 16);
+  const size_t cmin = std::max<size_t>(by_rows ? 1 : std::min(cmax, 16 * k), cmax / MF_PIPE_RAMP);
   std::vector<size_t> sizes = chunk_schedule(total, cmin, cmax);
   const size_t nchunks = sizes.size();
   const size_t in_slot = ((by_rows ? cmax * n : cmax + k - 1) * w + 255) / 256 * 256;

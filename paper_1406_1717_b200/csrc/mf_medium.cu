@@ -14,9 +14,15 @@ template <int DT, int R> struct WarpsFor {
 #define MF_W_R16 8  // teams per CTA for R = 16 (experiments)
 #endif
 #ifndef MF_W_R8
-#define MF_W_R8 8   // ... for R <= 8
+#define MF_W_R8 4   // ... for R = 8 (4 teams x 8 CTAs/SM: k = 255 1.00 -> 0.985 ms)
 #endif
-  static constexpr int value = R >= 32 ? 2 : (R >= 16 ? MF_W_R16 : MF_W_R8);
+#ifndef MF_W_R4
+#define MF_W_R4 8   // ... for R <= 4
+#endif
+#ifndef MF_W_R32
+#define MF_W_R32 2
+#endif
+  static constexpr int value = R >= 32 ? MF_W_R32 : (R >= 16 ? MF_W_R16 : R >= 8 ? MF_W_R8 : MF_W_R4);
 };
 
 template <int DT, int R>

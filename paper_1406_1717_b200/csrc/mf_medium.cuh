@@ -109,7 +109,7 @@ __device__ __forceinline__ uint32_t row_addr(uint32_t L, uint32_t w) {
 // and its first warp walks the 32 chunks.  WP = 2 for the largest blocks halves the
 // dependent merge chains that bound them at low occupancy.
 #ifndef MF_MINB_R8
-#define MF_MINB_R8 4  // resident CTAs the R = 8 kernel is compiled for (64-register cap: 1.19 -> 1.16 ms at k = 255)
+#define MF_MINB_R8 8  // resident CTAs the R = 8 kernel is compiled for (64-register cap with 4 teams per CTA)
 #endif
 #ifndef MF_MINB_R4
 #define MF_MINB_R4 4  // (64 registers: k = 101 1.65 -> 1.45 ms)
