@@ -33,8 +33,21 @@ namespace mf {
 // 128 threads so that two tiles of input still fit the shared-memory budget.
 template <int DT, int K> struct SmallShape {
   static constexpr bool wide = sizeof(typename Traits<DT>::U) == 8;
-  static constexpr int T = wide ? 128 : (K <= 5 ? 256 : K <= 7 ? 512 : K <= 23 ? 256 : 512);
-  static constexpr int UPT = wide ? (K <= 7 ? 4 : K <= 15 ? 2 : 1) : (K <= 5 ? 4 : K <= 11 ? 2 : 1);
+#ifndef MF_SMALL_T_K31
+#define MF_SMALL_T_K31 512  // (experiments: tile shape of k = 24..31, 32-bit keys)
+#endif
+#ifndef MF_SMALL_UPT_K31
+#define MF_SMALL_UPT_K31 1
+#endif
+#ifndef MF_SMALL_T_K3
+#define MF_SMALL_T_K3 256   // (experiments: tile shape of k <= 5, 32-bit keys)
+#endif
+#ifndef MF_SMALL_UPT_K3
+#define MF_SMALL_UPT_K3 4
+#endif
+  static constexpr int T = wide ? 128 : (K <= 5 ? MF_SMALL_T_K3 : K <= 7 ? 512 : K <= 23 ? 256 : MF_SMALL_T_K31);
+  static constexpr int UPT = wide ? (K <= 7 ? 4 : K <= 15 ? 2 : 1)
+                                  : (K <= 5 ? MF_SMALL_UPT_K3 : K <= 11 ? 2 : K <= 23 ? 1 : MF_SMALL_UPT_K31);
 };
 
 template <int DT, int K, int T>
