@@ -5,6 +5,10 @@
 #include "mf_launch.h"
 #include "mf_large.cuh"
 
+#ifndef MF_TILE_RADIX
+#define MF_TILE_RADIX 0  // 1: LSD radix tile sort, 0: comparison network + merge levels
+#endif
+
 namespace mf {
 
 namespace {
@@ -45,6 +49,8 @@ cudaError_t configure(const LargeGeom& L) {
   cudaError_t e = cudaSuccess;
   if (!done) {
     e = cudaFuncSetAttribute(ml_tile_sort<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TileSort<U>::smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(ml_tile_radix<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TileRadix<U>::smem);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(ml_merge_pass<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)merge_tile_smem<U>());
@@ -96,7 +102,13 @@ cudaError_t sort_blocks(const LargeGeom& L, unsigned char* ws, const Layout<DT>&
   cudaError_t e = configure<DT>(L);
   if (e != cudaSuccess) return e;
   E* bufs[2] = {reinterpret_cast<E*>(ws + lay.off_s0), reinterpret_cast<E*>(ws + lay.off_s1)};
+#if MF_TILE_RADIX
+  static_assert(TileRadix<U>::TS == TileSort<U>::TS, "tile size is shared with the merge passes");
+  ml_tile_radix<DT><<<dim3((unsigned)(L.nb * L.tiles), L.g.rows), TileRadix<U>::NT, TileRadix<U>::smem, s>>>(
+      L, bufs[0]);
+#else
   ml_tile_sort<DT><<<dim3((unsigned)(L.nb * L.tiles), L.g.rows), LNT, TileSort<U>::smem, s>>>(L, bufs[0]);
+#endif
   ++*launches;
   int cur = 0;
   uint2* splits = reinterpret_cast<uint2*>(ws + lay.off_split);

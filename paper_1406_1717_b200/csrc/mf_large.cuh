@@ -95,6 +95,188 @@ __global__ void __launch_bounds__(LNT, 3) ml_tile_sort(LargeGeom L, Elem<typenam
   for (uint32_t i = threadIdx.x; i < len; i += LNT) o[i] = s[pad<PS>(i)];
 }
 
+// ---- phase 1a (default): LSD radix sort of a TS-element tile in shared memory ----------
+// 8-bit digits, least significant first.  Every pass is stable, and the tile starts in
+// index order, so the result is the (key, index) order of E::less without ever comparing
+// indices: ~17 thread-instructions per element per pass instead of the ~350 of the
+// comparison network above.  Ranking is warp-level multisplit: each warp owns WS = 32R
+// consecutive positions, walks them in order (r-major, lane-minor) and ranks an element
+// among its warp's earlier same-digit elements with one match.any plus a warp-private
+// counter; a digit-major, warp-minor exclusive scan of the counters turns ranks into
+// positions.  Digits on which every key of the tile agrees are skipped (AND/OR test), so
+// the clustered keys of config 4 take fewer than 8 passes.
+template <typename U> struct TileRadixCfg;
+#ifndef MF_RADIX_NCH
+#define MF_RADIX_NCH 2  // interleaved ranking chains per warp
+#endif
+#ifndef MF_RADIX_MATCH
+#define MF_RADIX_MATCH 0  // 1: match.any.sync peers, 0: eight ballots
+#endif
+template <> struct TileRadixCfg<uint32_t> { static constexpr int NT = 512, R = 16, MINB = 2; };
+template <> struct TileRadixCfg<uint64_t> { static constexpr int NT = 256, R = 16, MINB = 3; };
+template <typename U> struct TileRadix {
+  static constexpr int NT = TileRadixCfg<U>::NT, R = TileRadixCfg<U>::R, W = NT / 32, MINB = TileRadixCfg<U>::MINB;
+  static constexpr int NCH = MF_RADIX_NCH, RC = R / NCH, VW = W * NCH;  // virtual warps: (warp, chain)
+  static constexpr int WS = 32 * R, TS = NT * R;
+  static_assert(R % NCH == 0, "chains split a thread's items evenly");
+  static constexpr size_t smem = sizeof(U) * TS + sizeof(uint16_t) * TS + sizeof(uint32_t) * (VW * 256 + 2 * W);
+};
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ uint32_t red_and(uint32_t v) { return __reduce_and_sync(0xFFFFFFFFu, v); }
+__device__ __forceinline__ uint32_t red_or(uint32_t v) { return __reduce_or_sync(0xFFFFFFFFu, v); }
+__device__ __forceinline__ uint64_t red_and(uint64_t v) {
+  return ((uint64_t)red_and((uint32_t)(v >> 32)) << 32) | red_and((uint32_t)v);
+}
+__device__ __forceinline__ uint64_t red_or(uint64_t v) {
+  return ((uint64_t)red_or((uint32_t)(v >> 32)) << 32) | red_or((uint32_t)v);
+}
+// lanes of the warp holding the same 8-bit digit
+__device__ __forceinline__ uint32_t peers8(uint32_t dg) {
+#if MF_RADIX_MATCH
+  return __match_any_sync(0xFFFFFFFFu, dg);
+#else
+  uint32_t m = 0xFFFFFFFFu;
+#pragma unroll
+  for (int bit = 0; bit < 8; ++bit) {
+    const bool p = (dg >> bit) & 1u;
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, p);
+    m &= p ? bal : ~bal;
+  }
+  return m;
+#endif
+}
+// full 16-byte stores for 64-bit keys: a partially written sector costs a DRAM fill read
+__device__ __forceinline__ void store_elem(Elem<uint32_t>* o, uint32_t key, uint32_t idx) {
+  *o = Elem<uint32_t>::make(key, idx);
+}
+__device__ __forceinline__ void store_elem(Elem<uint64_t>* o, uint64_t key, uint32_t idx) {
+  static_assert(sizeof(Elem<uint64_t>) == 16, "16-byte element");
+  *reinterpret_cast<uint4*>(o) = make_uint4((uint32_t)key, (uint32_t)(key >> 32), idx, 0u);
+}
+
+template <int DT>
+__global__ void __launch_bounds__(TileRadix<typename Traits<DT>::U>::NT, TileRadix<typename Traits<DT>::U>::MINB)
+    ml_tile_radix(LargeGeom L, Elem<typename Traits<DT>::U>* out) {
+  using Tr = Traits<DT>;
+  using U = typename Tr::U;
+  using TV = typename Tr::T;
+  using C = TileRadix<U>;
+  constexpr int R = C::R, W = C::W, WS = C::WS, TS = C::TS, NCH = C::NCH, RC = C::RC, VW = C::VW;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  U* sk = reinterpret_cast<U*>(smem_raw);
+  uint16_t* si = reinterpret_cast<uint16_t*>(sk + TS);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(si + TS);        // [VW][256]
+  uint32_t* wtot = hist + VW * 256;                              // [2W]: digit-total scan
+  const Geom& g = L.g;
+  const uint64_t row = blockIdx.y;
+  const uint64_t b = blockIdx.x / L.tiles;
+  const uint32_t t = blockIdx.x % L.tiles;
+  const TV* x = reinterpret_cast<const TV*>(g.x) + row * g.ld_x;
+  const uint32_t k = g.k;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t base = warp * WS + lane;                        // position of item r: base + 32r
+  U key[R];
+  uint32_t rix[R];                                               // index (low 16) | rank (high 16)
+  U kand = UMax<U>::v, kor = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t e = t * TS + base + 32 * r;
+    const uint64_t gp = b * k + e;
+    key[r] = (e < k && gp < g.n) ? Tr::enc(__ldg(x + gp)) : UMax<U>::v;
+    rix[r] = base + 32 * r;
+    kand &= key[r];
+    kor |= key[r];
+  }
+  // which digits vary inside the tile
+  kand = red_and(kand);
+  kor = red_or(kor);
+  U* wred = reinterpret_cast<U*>(hist);                          // scratch before the first pass
+  if (lane == 0) { wred[2 * warp] = kand; wred[2 * warp + 1] = kor; }
+  __syncthreads();
+  U diff = 0;
+  {
+    U a = UMax<U>::v, o = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) { a &= wred[2 * w]; o |= wred[2 * w + 1]; }
+    diff = a ^ o;
+  }
+  __syncthreads();
+  // chain c of this warp ranks items r = c*RC .. c*RC+RC-1 against its own counters; the
+  // chains are independent, so their shared-memory read -> write round trips overlap
+  uint32_t* hw = hist + warp * NCH * 256;
+  const uint32_t lt = lanemask_lt();
+#pragma unroll 1
+  for (int d = 0; d < (int)(8 * sizeof(U)); d += 8) {
+    if (((diff >> d) & 0xFF) == 0) continue;                    // uniform across the CTA
+#pragma unroll
+    for (int j = 0; j < 8 * NCH; ++j) hw[lane + 32 * j] = 0;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < RC; ++j) {
+      uint32_t dg[NCH], peers[NCH], before[NCH], cnt[NCH];
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        dg[c] = (uint32_t)(key[c * RC + j] >> d) & 0xFFu;
+        peers[c] = peers8(dg[c]);
+        before[c] = __popc(peers[c] & lt);
+        cnt[c] = hw[c * 256 + dg[c]];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        if (before[c] == 0) hw[c * 256 + dg[c]] = cnt[c] + __popc(peers[c]);
+        rix[c * RC + j] = (rix[c * RC + j] & 0xFFFFu) | ((cnt[c] + before[c]) << 16);
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    if (threadIdx.x < 256) {                                     // digit-major, virtual-warp-minor scan
+      const uint32_t dgt = threadIdx.x;
+      uint32_t sum = 0;
+#pragma unroll 8
+      for (int v = 0; v < VW; ++v) { const uint32_t c = hist[v * 256 + dgt]; hist[v * 256 + dgt] = sum; sum += c; }
+      uint32_t inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (lane >= (uint32_t)o) inc += v;
+      }
+      if (lane == 31) wtot[warp] = inc;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      uint32_t pre = inc - sum;
+      for (uint32_t w = 0; w < warp; ++w) pre += wtot[w];
+#pragma unroll 8
+      for (int v = 0; v < VW; ++v) hist[v * 256 + dgt] += pre;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t dgr = (uint32_t)(key[r] >> d) & 0xFFu;
+      const uint32_t pos = hw[(r / RC) * 256 + dgr] + (rix[r] >> 16);
+      sk[pos] = key[r];
+      si[pos] = (uint16_t)rix[r];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      key[r] = sk[base + 32 * r];
+      rix[r] = si[base + 32 * r];
+    }
+  }
+  const uint32_t len = min((uint32_t)TS, k - t * TS);
+  Elem<U>* o = out + (row * L.nb + b) * k + (uint64_t)t * TS;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t p = base + 32 * r;
+    if (p < len) store_elem(o + p, key[r], t * TS + (rix[r] & 0xFFFFu));
+  }
+}
+
 // Warp-cooperative merge-path split: the number of X elements among the first d merged
 // elements of X[0,lx) and Y[0,ly) under `before(x, y)` (x goes first).  Each round probes
 // 32 diagonal points at once, so a split over 10^5 costs 4 rounds of loads, not 17.
@@ -286,15 +468,18 @@ __global__ void __launch_bounds__(LNT, 4) ml_unit_merge(LargeGeom L, const Elem<
   const int dd = threadIdx.x * LR2;
   uint2* ro = rab + ug * (uint64_t)L.C * L.CL;
   __syncthreads();
-  U* sk = reinterpret_cast<U*>(s);                          // staging: keys, then origins
-  uint32_t* so = reinterpret_cast<uint32_t*>(sk + LQ);
+  // staging: keys, then origins, both padded (pad<LPS>): a thread's LR2 consecutive slots
+  // would otherwise put every other lane on the same bank (16-way conflicts)
+  static_assert((sizeof(U) + 4) * (LQ + (LQ >> LPS)) <= merge_tile_smem<U>(), "staging fits the merge tile");
+  U* sk = reinterpret_cast<U*>(s);
+  uint32_t* so = reinterpret_cast<uint32_t*>(sk + LQ + (LQ >> LPS));
 #pragma unroll
   for (int r = 0; r < LR2; ++r) {
     if (r < cnt) {
       const uint32_t q = d0 + dd + r;
       const uint32_t idx = v[r].idx();
-      sk[dd + r] = v[r].key();
-      so[dd + r] = idx | (srcB[r] ? 0x80000000u : 0u);
+      sk[pad<LPS>(dd + r)] = v[r].key();
+      so[pad<LPS>(dd + r)] = idx | (srcB[r] ? 0x80000000u : 0u);
       uint2* slot = ro + (uint64_t)(idx & (L.CL - 1)) * C + (idx >> L.CLshift);  // transposed [t][c]
       if (srcB[r]) slot->y = q; else slot->x = q;
       const uint32_t sw = (dd + r) >> 10;                   // superword within the tile
@@ -304,15 +489,9 @@ __global__ void __launch_bounds__(LNT, 4) ml_unit_merge(LargeGeom L, const Elem<
   __syncthreads();
   U* mko = mk + ug * L.nqp + d0;
   uint32_t* oo = org + ug * L.nqp + d0;
-  {  // 16-byte copies (d0 and the unit stride nqp are multiples of 32 elements)
-    constexpr uint32_t KV = 16 / sizeof(U);
-    const uint32_t nv = (d1 - d0) / 4, nk = (d1 - d0) / KV;
-    for (uint32_t i = threadIdx.x; i < nk; i += LNT)
-      reinterpret_cast<uint4*>(mko)[i] = reinterpret_cast<const uint4*>(sk)[i];
-    for (uint32_t i = threadIdx.x; i < nv; i += LNT)
-      reinterpret_cast<uint4*>(oo)[i] = reinterpret_cast<const uint4*>(so)[i];
-    for (uint32_t i = nk * KV + threadIdx.x; i < d1 - d0; i += LNT) mko[i] = sk[i];
-    for (uint32_t i = nv * 4 + threadIdx.x; i < d1 - d0; i += LNT) oo[i] = so[i];
+  for (uint32_t i = threadIdx.x; i < d1 - d0; i += LNT) {
+    mko[i] = sk[pad<LPS>(i)];
+    oo[i] = so[pad<LPS>(i)];
   }
   // live count of each superword at every chunk start c: A elements with chunk >= c plus
   // B elements with chunk < c.  One warp per superword; lanes scan 32 chunks at a time.
