@@ -95,31 +95,26 @@ __global__ void __launch_bounds__(LNT, 3) ml_tile_sort(LargeGeom L, Elem<typenam
   for (uint32_t i = threadIdx.x; i < len; i += LNT) o[i] = s[pad<PS>(i)];
 }
 
-// ---- phase 1a (default): LSD radix sort of a TS-element tile in shared memory ----------
-// 8-bit digits, least significant first.  Every pass is stable, and the tile starts in
-// index order, so the result is the (key, index) order of E::less without ever comparing
-// indices: ~17 thread-instructions per element per pass instead of the ~350 of the
-// comparison network above.  Ranking is warp-level multisplit: each warp owns WS = 32R
-// consecutive positions, walks them in order (r-major, lane-minor) and ranks an element
-// among its warp's earlier same-digit elements with one match.any plus a warp-private
-// counter; a digit-major, warp-minor exclusive scan of the counters turns ranks into
-// positions.  Digits on which every key of the tile agrees are skipped (AND/OR test), so
-// the clustered keys of config 4 take fewer than 8 passes.
+// ---- phase 1a (experiment, MF_TILE_RADIX=1): LSD radix sort of a TS-element tile ------
+// 5-bit digits, least significant first.  Every pass is stable and the tile starts in index
+// order, so the result is the (key, index) order of E::less without comparing indices.
+// Ranking is warp-level multisplit with the 32 bin counters in registers, one bin per
+// lane: five ballots give each lane the mask of lanes holding its bin, a shuffle from lane
+// `digit` gives an element its peers and the running count of its bin, so no pass has a
+// shared-memory read -> write chain.  A bin-major, warp-minor exclusive scan of the NB x W
+// warp totals turns ranks into positions.  Digits on which every key of the tile agrees are
+// skipped (AND/OR test).  (Measured: 8-bit digits with warp counters in shared memory were
+// slower than the comparison network, with match.any or with ballots.)
 template <typename U> struct TileRadixCfg;
-#ifndef MF_RADIX_NCH
-#define MF_RADIX_NCH 2  // interleaved ranking chains per warp
-#endif
-#ifndef MF_RADIX_MATCH
-#define MF_RADIX_MATCH 0  // 1: match.any.sync peers, 0: eight ballots
-#endif
-template <> struct TileRadixCfg<uint32_t> { static constexpr int NT = 512, R = 16, MINB = 2; };
+template <> struct TileRadixCfg<uint32_t> { static constexpr int NT = 1024, R = 8, MINB = 1; };
 template <> struct TileRadixCfg<uint64_t> { static constexpr int NT = 256, R = 16, MINB = 3; };
 template <typename U> struct TileRadix {
   static constexpr int NT = TileRadixCfg<U>::NT, R = TileRadixCfg<U>::R, W = NT / 32, MINB = TileRadixCfg<U>::MINB;
-  static constexpr int NCH = MF_RADIX_NCH, RC = R / NCH, VW = W * NCH;  // virtual warps: (warp, chain)
+  static constexpr int DB = 5, NB = 1 << DB;
   static constexpr int WS = 32 * R, TS = NT * R;
-  static_assert(R % NCH == 0, "chains split a thread's items evenly");
-  static constexpr size_t smem = sizeof(U) * TS + sizeof(uint16_t) * TS + sizeof(uint32_t) * (VW * 256 + 2 * W);
+  static_assert(NB * W == NT, "one scan entry (bin, warp) per thread");
+  static constexpr size_t smem = sizeof(U) * TS + sizeof(uint16_t) * TS + sizeof(uint32_t) * NT +
+                                 sizeof(U) * 2 * W + sizeof(uint32_t) * W;
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -134,21 +129,6 @@ __device__ __forceinline__ uint64_t red_and(uint64_t v) {
 }
 __device__ __forceinline__ uint64_t red_or(uint64_t v) {
   return ((uint64_t)red_or((uint32_t)(v >> 32)) << 32) | red_or((uint32_t)v);
-}
-// lanes of the warp holding the same 8-bit digit
-__device__ __forceinline__ uint32_t peers8(uint32_t dg) {
-#if MF_RADIX_MATCH
-  return __match_any_sync(0xFFFFFFFFu, dg);
-#else
-  uint32_t m = 0xFFFFFFFFu;
-#pragma unroll
-  for (int bit = 0; bit < 8; ++bit) {
-    const bool p = (dg >> bit) & 1u;
-    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, p);
-    m &= p ? bal : ~bal;
-  }
-  return m;
-#endif
 }
 // full 16-byte stores for 64-bit keys: a partially written sector costs a DRAM fill read
 __device__ __forceinline__ void store_elem(Elem<uint32_t>* o, uint32_t key, uint32_t idx) {
@@ -166,12 +146,13 @@ __global__ void __launch_bounds__(TileRadix<typename Traits<DT>::U>::NT, TileRad
   using U = typename Tr::U;
   using TV = typename Tr::T;
   using C = TileRadix<U>;
-  constexpr int R = C::R, W = C::W, WS = C::WS, TS = C::TS, NCH = C::NCH, RC = C::RC, VW = C::VW;
+  constexpr int R = C::R, W = C::W, WS = C::WS, TS = C::TS, DB = C::DB, NB = C::NB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   U* sk = reinterpret_cast<U*>(smem_raw);
   uint16_t* si = reinterpret_cast<uint16_t*>(sk + TS);
-  uint32_t* hist = reinterpret_cast<uint32_t*>(si + TS);        // [VW][256]
-  uint32_t* wtot = hist + VW * 256;                              // [2W]: digit-total scan
+  uint32_t* tot = reinterpret_cast<uint32_t*>(si + TS);         // [NB][W] warp totals -> bases
+  U* wred = reinterpret_cast<U*>(tot + C::NT);                   // [W][2] AND / OR
+  uint32_t* wsum = reinterpret_cast<uint32_t*>(wred + 2 * W);    // [W] scan carries
   const Geom& g = L.g;
   const uint64_t row = blockIdx.y;
   const uint64_t b = blockIdx.x / L.tiles;
@@ -192,10 +173,8 @@ __global__ void __launch_bounds__(TileRadix<typename Traits<DT>::U>::NT, TileRad
     kand &= key[r];
     kor |= key[r];
   }
-  // which digits vary inside the tile
   kand = red_and(kand);
   kor = red_or(kor);
-  U* wred = reinterpret_cast<U*>(hist);                          // scratch before the first pass
   if (lane == 0) { wred[2 * warp] = kand; wred[2 * warp + 1] = kor; }
   __syncthreads();
   U diff = 0;
@@ -203,61 +182,49 @@ __global__ void __launch_bounds__(TileRadix<typename Traits<DT>::U>::NT, TileRad
     U a = UMax<U>::v, o = 0;
 #pragma unroll
     for (int w = 0; w < W; ++w) { a &= wred[2 * w]; o |= wred[2 * w + 1]; }
-    diff = a ^ o;
+    diff = a ^ o;                                                // bits that vary in the tile
   }
-  __syncthreads();
-  // chain c of this warp ranks items r = c*RC .. c*RC+RC-1 against its own counters; the
-  // chains are independent, so their shared-memory read -> write round trips overlap
-  uint32_t* hw = hist + warp * NCH * 256;
   const uint32_t lt = lanemask_lt();
+  uint32_t xm[DB];                                               // ~0 where this lane's bin has a 0 bit
+#pragma unroll
+  for (int bit = 0; bit < DB; ++bit) xm[bit] = ((lane >> bit) & 1u) ? 0u : 0xFFFFFFFFu;
 #pragma unroll 1
-  for (int d = 0; d < (int)(8 * sizeof(U)); d += 8) {
-    if (((diff >> d) & 0xFF) == 0) continue;                    // uniform across the CTA
-#pragma unroll
-    for (int j = 0; j < 8 * NCH; ++j) hw[lane + 32 * j] = 0;
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < RC; ++j) {
-      uint32_t dg[NCH], peers[NCH], before[NCH], cnt[NCH];
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        dg[c] = (uint32_t)(key[c * RC + j] >> d) & 0xFFu;
-        peers[c] = peers8(dg[c]);
-        before[c] = __popc(peers[c] & lt);
-        cnt[c] = hw[c * 256 + dg[c]];
-      }
-      __syncwarp();
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        if (before[c] == 0) hw[c * 256 + dg[c]] = cnt[c] + __popc(peers[c]);
-        rix[c * RC + j] = (rix[c * RC + j] & 0xFFFFu) | ((cnt[c] + before[c]) << 16);
-      }
-      __syncwarp();
-    }
-    __syncthreads();
-    if (threadIdx.x < 256) {                                     // digit-major, virtual-warp-minor scan
-      const uint32_t dgt = threadIdx.x;
-      uint32_t sum = 0;
-#pragma unroll 8
-      for (int v = 0; v < VW; ++v) { const uint32_t c = hist[v * 256 + dgt]; hist[v * 256 + dgt] = sum; sum += c; }
-      uint32_t inc = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, inc, o);
-        if (lane >= (uint32_t)o) inc += v;
-      }
-      if (lane == 31) wtot[warp] = inc;
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      uint32_t pre = inc - sum;
-      for (uint32_t w = 0; w < warp; ++w) pre += wtot[w];
-#pragma unroll 8
-      for (int v = 0; v < VW; ++v) hist[v * 256 + dgt] += pre;
-    }
-    __syncthreads();
+  for (int d = 0; d < (int)(8 * sizeof(U)); d += DB) {
+    if (((diff >> d) & (NB - 1)) == 0) continue;                // uniform across the CTA
+    uint32_t cnt = 0;                                            // this warp's count of bin `lane`
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const uint32_t dgr = (uint32_t)(key[r] >> d) & 0xFFu;
-      const uint32_t pos = hw[(r / RC) * 256 + dgr] + (rix[r] >> 16);
+      const uint32_t dg = (uint32_t)(key[r] >> d) & (NB - 1);
+      uint32_t m = 0xFFFFFFFFu;                                  // lanes whose digit is `lane`
+#pragma unroll
+      for (int bit = 0; bit < DB; ++bit) m &= __ballot_sync(0xFFFFFFFFu, (dg >> bit) & 1u) ^ xm[bit];
+      const uint32_t peers = __shfl_sync(0xFFFFFFFFu, m, dg);
+      const uint32_t cb = __shfl_sync(0xFFFFFFFFu, cnt, dg);
+      rix[r] = (rix[r] & 0xFFFFu) | ((cb + __popc(peers & lt)) << 16);
+      cnt += __popc(m);
+    }
+    tot[lane * W + warp] = cnt;
+    __syncthreads();
+    {  // exclusive scan of tot in (bin, warp) order, one entry per thread
+      const uint32_t v = tot[threadIdx.x];
+      uint32_t inc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (lane >= (uint32_t)o) inc += y;
+      }
+      if (lane == 31) wsum[warp] = inc;
+      __syncthreads();
+      uint32_t pre = inc - v;
+      for (uint32_t w = 0; w < warp; ++w) pre += wsum[w];
+      tot[threadIdx.x] = pre;
+    }
+    __syncthreads();
+    const uint32_t bw = tot[lane * W + warp];                    // this warp's base of bin `lane`
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t dg = (uint32_t)(key[r] >> d) & (NB - 1);
+      const uint32_t pos = __shfl_sync(0xFFFFFFFFu, bw, dg) + (rix[r] >> 16);
       sk[pos] = key[r];
       si[pos] = (uint16_t)rix[r];
     }
