@@ -37,7 +37,7 @@ cudaError_t launch_k(const Geom& g, cudaStream_t s) {
 // With k = 3 the paper's blocks hold three samples and every window spans two blocks, so the
 // sort + Figure-7 walk degenerate to one compare-exchange chain per output: the median of
 // (x[i], x[i+1], x[i+2]) under the sample order is max(min(a, b), min(max(a, b), c)) on the
-// ordered keys (mf_common.cuh).  The result is the same sample the reference picks (equal
+// signed keys below.  The result is the same sample the reference picks (equal
 // keys are equal bit patterns, so tie-breaking cannot change the emitted value), at ~4 key
 // ops per output, so the kernel streams at HBM speed.  A warp owns 32*Q 16-byte groups of
 // consecutive outputs; its Q loads and Q stores are each one contiguous 512-byte run, and a
@@ -55,6 +55,34 @@ constexpr int kMed3Threads = 256;
 #endif
 constexpr int kMed3Q = MF_MED3_Q, kMed3CtasPerSm = MF_MED3_CTAS;
 
+// Signed keys: an involution on the sample bits whose signed order is the sample order
+// (floats map negative patterns through x ^ 0x7F..F; integers are their own
+// key), so one shift + one LOP3 encodes and the same two decode.
+template <int DT> struct SKey;
+template <> struct SKey<DT_I32> {
+  using S = int32_t;
+  __device__ __forceinline__ static S f(int32_t v) { return v; }
+  __device__ __forceinline__ static int32_t g(S s) { return s; }
+};
+template <> struct SKey<DT_I64> {
+  using S = int64_t;
+  __device__ __forceinline__ static S f(int64_t v) { return v; }
+  __device__ __forceinline__ static int64_t g(S s) { return s; }
+};
+template <> struct SKey<DT_F32> {
+  using S = int32_t;
+  __device__ __forceinline__ static S f(uint32_t b) { const S s = (S)b; return s ^ ((s >> 31) & 0x7FFFFFFF); }
+  __device__ __forceinline__ static uint32_t g(S s) { return (uint32_t)(s ^ ((s >> 31) & 0x7FFFFFFF)); }
+};
+template <> struct SKey<DT_F64> {
+  using S = int64_t;
+  __device__ __forceinline__ static S f(uint64_t b) {
+    const S s = (S)b;
+    return s ^ ((s >> 63) & 0x7FFFFFFFFFFFFFFFll);
+  }
+  __device__ __forceinline__ static uint64_t g(S s) { return (uint64_t)(s ^ ((s >> 63) & 0x7FFFFFFFFFFFFFFFll)); }
+};
+
 template <typename U>
 __device__ __forceinline__ U med3(U a, U b, U c) {
   const U lo = a < b ? a : b, hi = a < b ? b : a;
@@ -64,9 +92,9 @@ __device__ __forceinline__ U med3(U a, U b, U c) {
 
 template <int DT>
 __global__ void __launch_bounds__(kMed3Threads) mf_med3_kernel(Geom g, uint64_t cpr, bool vec) {
-  using Tr = Traits<DT>;
-  using T = typename Tr::T;
-  using U = typename Tr::U;
+  using T = typename Traits<DT>::T;
+  using K = SKey<DT>;
+  using U = typename K::S;
   constexpr int E4 = 16 / sizeof(T), Q = kMed3Q;
   constexpr uint64_t WSPAN = 32ull * Q * E4, SPAN = WSPAN * (kMed3Threads / 32);
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -100,17 +128,17 @@ __global__ void __launch_bounds__(kMed3Threads) mf_med3_kernel(Geom g, uint64_t 
           v[E4 + 1] = n1;
           U kk[E4 + 2];
 #pragma unroll
-          for (int i = 0; i < E4 + 2; ++i) kk[i] = Tr::enc(v[i]);
+          for (int i = 0; i < E4 + 2; ++i) kk[i] = K::f(v[i]);
           T out[E4];
 #pragma unroll
-          for (int i = 0; i < E4; ++i) out[i] = Tr::dec(med3<U>(kk[i], kk[i + 1], kk[i + 2]));
+          for (int i = 0; i < E4; ++i) out[i] = K::g(med3<U>(kk[i], kk[i + 1], kk[i + 2]));
           uint4 o;
           memcpy(&o, &out[0], 16);
           reinterpret_cast<uint4*>(y + wb)[j * 32 + lane] = o;
         }
       } else {                                                     // ragged tail or unaligned rows
         for (uint64_t o = wb + lane; o < min(wb + WSPAN, g.keep); o += 32)
-          y[o] = Tr::dec(med3<U>(Tr::enc(__ldg(x + o)), Tr::enc(__ldg(x + o + 1)), Tr::enc(__ldg(x + o + 2))));
+          y[o] = K::g(med3<U>(K::f(__ldg(x + o)), K::f(__ldg(x + o + 1)), K::f(__ldg(x + o + 2))));
       }
     }
   }
