@@ -8,6 +8,8 @@ import paper_1406_1717_b200 as mf  # noqa: E402
 cfg = os.environ.get("CFG", "c2")
 if cfg == "c2":
     x = mf.generate_device("uniform_f32", 2, 1 << 26)
+elif cfg == "c1":
+    x = mf.generate_device("uniform_f64", 1, 1_000_000)
 elif cfg == "c4":
     x = torch.from_numpy(mf.generate_trend_f64(4, 1 << 27)).cuda()
 else:  # c5
