@@ -5,6 +5,9 @@
 #include "mf_launch.h"
 #include "mf_large.cuh"
 
+#ifndef MF_LARGE_KEYORD
+#define MF_LARGE_KEYORD 1  // the filter's block sort compares keys only (the phase API never does)
+#endif
 #ifndef MF_TILE_RADIX
 #define MF_TILE_RADIX 0  // 1: LSD radix tile sort, 0: comparison network + merge levels
 #endif
@@ -48,13 +51,16 @@ cudaError_t configure(const LargeGeom& L) {
   static size_t unit_merge_set = 0;
   cudaError_t e = cudaSuccess;
   if (!done) {
-    e = cudaFuncSetAttribute(ml_tile_sort<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TileSort<U>::smem);
-    if (e != cudaSuccess) return e;
+    for (auto f : {ml_tile_sort<DT, true>, ml_tile_sort<DT, false>}) {
+      e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TileSort<U>::smem);
+      if (e != cudaSuccess) return e;
+    }
     e = cudaFuncSetAttribute(ml_tile_radix<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TileRadix<U>::smem);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(ml_merge_pass<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)merge_tile_smem<U>());
-    if (e != cudaSuccess) return e;
+    for (auto f : {ml_merge_pass<DT, true>, ml_merge_pass<DT, false>}) {
+      e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)merge_tile_smem<U>());
+      if (e != cudaSuccess) return e;
+    }
     e = cudaFuncSetAttribute(ml_walk<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(sizeof(U) * 32 * 9 * (LNT / 32)));
     if (e != cudaSuccess) return e;
@@ -93,8 +99,9 @@ struct Layout {
   }
 };
 
-// Segmented sort of every block into (key, index) order; returns the buffer holding it.
-template <int DT>
+// Segmented sort of every block into key order (KO) or (key, index) order; returns the
+// buffer holding it.
+template <int DT, bool KO>
 cudaError_t sort_blocks(const LargeGeom& L, unsigned char* ws, const Layout<DT>& lay, cudaStream_t s,
                         uint64_t* launches, Elem<typename Traits<DT>::U>** result) {
   using U = typename Traits<DT>::U;
@@ -107,16 +114,16 @@ cudaError_t sort_blocks(const LargeGeom& L, unsigned char* ws, const Layout<DT>&
   ml_tile_radix<DT><<<dim3((unsigned)(L.nb * L.tiles), L.g.rows), TileRadix<U>::NT, TileRadix<U>::smem, s>>>(
       L, bufs[0]);
 #else
-  ml_tile_sort<DT><<<dim3((unsigned)(L.nb * L.tiles), L.g.rows), LNT, TileSort<U>::smem, s>>>(L, bufs[0]);
+  ml_tile_sort<DT, KO><<<dim3((unsigned)(L.nb * L.tiles), L.g.rows), LNT, TileSort<U>::smem, s>>>(L, bufs[0]);
 #endif
   ++*launches;
   int cur = 0;
   uint2* splits = reinterpret_cast<uint2*>(ws + lay.off_split);
   const uint64_t ptiles = (uint64_t)L.g.rows * L.nb * L.mtiles;
   for (uint64_t run = L.TS; run < L.g.k; run *= 2) {
-    ml_partition_pass<DT><<<(unsigned)((ptiles + 127) / 128), 128, 0, s>>>(L, bufs[cur], splits, (uint32_t)run,
+    ml_partition_pass<DT, KO><<<(unsigned)((ptiles + 127) / 128), 128, 0, s>>>(L, bufs[cur], splits, (uint32_t)run,
                                                                          ptiles);
-    ml_merge_pass<DT><<<dim3((unsigned)(L.nb * L.mtiles), L.g.rows), LNT, merge_tile_smem<U>(), s>>>(
+    ml_merge_pass<DT, KO><<<dim3((unsigned)(L.nb * L.mtiles), L.g.rows), LNT, merge_tile_smem<U>(), s>>>(
         L, bufs[cur], bufs[cur ^ 1], (uint32_t)run, splits);
     *launches += 2;
     cur ^= 1;
@@ -133,7 +140,7 @@ cudaError_t run_large_dt(const Geom& g, void* wsv, size_t ws_bytes, cudaStream_t
   unsigned char* ws = static_cast<unsigned char*>(wsv);
   using U = typename Traits<DT>::U;
   Elem<U>* sorted = nullptr;
-  cudaError_t e = sort_blocks<DT>(L, ws, lay, s, launches, &sorted);
+  cudaError_t e = sort_blocks<DT, MF_LARGE_KEYORD != 0>(L, ws, lay, s, launches, &sorted);
   if (e != cudaSuccess) return e;
   U* mk = reinterpret_cast<U*>(ws + lay.off_mk);
   uint32_t* org = reinterpret_cast<uint32_t*>(ws + lay.off_org);
@@ -167,7 +174,7 @@ cudaError_t run_sort_dt(const Geom& g, uint64_t nb, void* wsv, uint32_t* perm, c
   const Layout<DT> lay(L, true);
   using U = typename Traits<DT>::U;
   Elem<U>* sorted = nullptr;
-  cudaError_t e = sort_blocks<DT>(L, static_cast<unsigned char*>(wsv), lay, s, launches, &sorted);
+  cudaError_t e = sort_blocks<DT, false>(L, static_cast<unsigned char*>(wsv), lay, s, launches, &sorted);
   if (e != cudaSuccess) return e;
   const uint64_t total = (uint64_t)g.rows * nb * g.k;
   ml_extract_perm<DT><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(L, sorted, perm, total);

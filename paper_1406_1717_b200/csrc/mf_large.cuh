@@ -40,7 +40,7 @@ template <typename U> struct TileSort {
   static constexpr int R = TileSortCfg<U>::R;
   static constexpr int PS = pad_shift<R>();
   static constexpr int TS = 8 * 32 * R;
-  static constexpr size_t smem = sizeof(Elem<U>) * (TS + (TS >> PS) + 1);
+  static constexpr size_t smem = sizeof(Elem<U>) * (TS + (TS >> PS) + 1) + sizeof(uint32_t) * (LNT / 32);
 };
 
 struct LargeGeom {
@@ -58,12 +58,20 @@ struct LargeGeom {
   uint32_t NS;        // superwords (1024 positions) per unit
 };
 
+// Sort element of the large-k passes.  The filter sorts by key only (KO: equal keys in any
+// order, which no emitted median depends on; KElem* keep Elem's memory layout and compare
+// one key instead of (key, index)); the phase API (mf_block_sort_*) needs piecewise_sort's
+// exact permutation and sorts by (key, index).
+template <typename U, bool KO> using SortElem = std::conditional_t<KO, typename KeyOrd<U>::E, Elem<U>>;
+
 // ---- phase 1a: sort TS-element tiles of every block ----------------------------------
-template <int DT>
-__global__ void __launch_bounds__(LNT, 3) ml_tile_sort(LargeGeom L, Elem<typename Traits<DT>::U>* out) {
+template <int DT, bool KO>
+__global__ void __launch_bounds__(LNT, 3) ml_tile_sort(LargeGeom L, Elem<typename Traits<DT>::U>* out_) {
   using Tr = Traits<DT>;
   using U = typename Tr::U;
-  using E = Elem<U>;
+  using E = SortElem<U, KO>;
+  static_assert(sizeof(E) == sizeof(Elem<U>), "same memory layout");
+  E* out = reinterpret_cast<E*>(out_);
   using TV = typename Tr::T;
   using C = TileSort<U>;
   constexpr int R = C::R, PS = C::PS, TS = C::TS;
@@ -92,7 +100,34 @@ __global__ void __launch_bounds__(LNT, 3) ml_tile_sort(LargeGeom L, Elem<typenam
   merge_levels<E, R, PS, true>(s, 0, threadIdx.x, 32 * R, TS, v);
   const uint32_t len = min((uint32_t)TS, k - t * TS);
   E* o = out + (row * L.nb + b) * k + (uint64_t)t * TS;
-  for (uint32_t i = threadIdx.x; i < len; i += LNT) o[i] = s[pad<PS>(i)];
+  if (E::kFull || len == (uint32_t)TS) {
+    for (uint32_t i = threadIdx.x; i < len; i += LNT) o[i] = s[pad<PS>(i)];
+    return;
+  }
+  // Key order leaves the slot fillers past the block's end (index >= k, key UKEY_MAX) mixed
+  // with real UKEY_MAX elements: keep only real elements, in sorted order (stable
+  // compaction; one thread per run of TS / LNT positions, CTA scan of the run counts).
+  constexpr int RUN = TS / LNT;
+  uint32_t* wsum = reinterpret_cast<uint32_t*>(s + TS + (TS >> PS) + 1);  // past the tile
+  const uint32_t i0 = threadIdx.x * RUN;
+  uint32_t c = 0;
+#pragma unroll 4
+  for (int j = 0; j < RUN; ++j) c += s[pad<PS>(i0 + j)].idx() < k;
+  uint32_t inc = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+    if (lane >= (uint32_t)d) inc += y;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  uint32_t q = inc - c;
+  for (uint32_t w = 0; w < warp; ++w) q += wsum[w];
+#pragma unroll 4
+  for (int j = 0; j < RUN; ++j) {
+    const E e = s[pad<PS>(i0 + j)];
+    if (e.idx() < k) o[q++] = e;
+  }
 }
 
 // ---- phase 1a (experiment, MF_TILE_RADIX=1): LSD radix sort of a TS-element tile ------
@@ -331,10 +366,11 @@ __device__ __forceinline__ uint32_t merge_split(const E* X, uint32_t lx, const E
 
 // ---- merge-path partitions: the (start, end) split of every merge tile, computed up front
 // by one thread per tile so the merge kernels start streaming immediately ---------------
-template <int DT>
-__global__ void ml_partition_pass(LargeGeom L, const Elem<typename Traits<DT>::U>* in, uint2* splits, uint32_t run,
+template <int DT, bool KO>
+__global__ void ml_partition_pass(LargeGeom L, const Elem<typename Traits<DT>::U>* in_, uint2* splits, uint32_t run,
                                   uint64_t total) {
-  using E = Elem<typename Traits<DT>::U>;
+  using E = SortElem<typename Traits<DT>::U, KO>;
+  const E* in = reinterpret_cast<const E*>(in_);
   const uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= total) return;
   const uint32_t t = id % L.mtiles;
@@ -370,12 +406,14 @@ __global__ void ml_partition_units(LargeGeom L, const Elem<typename Traits<DT>::
 }
 
 // ---- phase 1b: one global merge pass (runs of length `run` within every block) --------
-template <int DT>
-__global__ void __launch_bounds__(LNT) ml_merge_pass(LargeGeom L, const Elem<typename Traits<DT>::U>* in,
-                                                     Elem<typename Traits<DT>::U>* out, uint32_t run,
+template <int DT, bool KO>
+__global__ void __launch_bounds__(LNT) ml_merge_pass(LargeGeom L, const Elem<typename Traits<DT>::U>* in_,
+                                                     Elem<typename Traits<DT>::U>* out_, uint32_t run,
                                                      const uint2* splits) {
   using U = typename Traits<DT>::U;
-  using E = Elem<U>;
+  using E = SortElem<U, KO>;
+  const E* in = reinterpret_cast<const E*>(in_);
+  E* out = reinterpret_cast<E*>(out_);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   E* s = reinterpret_cast<E*>(smem_raw);
   const uint64_t row = blockIdx.y;

@@ -196,6 +196,15 @@ __device__ __forceinline__ Elem<uint64_t> ldg_elem(const Elem<uint64_t>* p) {
   r.i = __ldg(&p->i);
   return r;
 }
+__device__ __forceinline__ KElem32 ldg_elem(const KElem32* p) {
+  KElem32 r; r.v = __ldg(reinterpret_cast<const unsigned long long*>(&p->v)); return r;
+}
+__device__ __forceinline__ KElem64 ldg_elem(const KElem64* p) {
+  KElem64 r;
+  r.k = __ldg(reinterpret_cast<const unsigned long long*>(&p->k));
+  r.i = __ldg(&p->i);
+  return r;
+}
 
 template <int K, int I, typename E>
 __device__ __forceinline__ void net_apply(E* v) {
