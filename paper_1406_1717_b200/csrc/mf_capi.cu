@@ -53,8 +53,8 @@ mf_status grow(void** p, size_t* cap, size_t need) {
   return MF_OK;
 }
 
-int class_for(mf_dtype, size_t k) {
-  if (k <= mf::kSmallMaxK) return MF_CLASS_SMALL;
+int class_for(mf_dtype dtype, size_t k) {
+  if (k <= mf::small_max_k(dtype)) return MF_CLASS_SMALL;
   if (k <= mf::kMediumMaxK) return MF_CLASS_MEDIUM;
   return MF_CLASS_LARGE;
 }
@@ -75,7 +75,7 @@ mf_status run_rows(mf_context* ctx, mf_dtype dtype, const void* d_x, size_t rows
   g.k = (uint32_t)k; g.h = (uint32_t)((k - 1) / 2);
   g.keep = keep; g.units = (keep + k - 1) / k; g.rows = (uint32_t)rows;
   int cls = ctx->force_class == MF_CLASS_AUTO ? class_for(dtype, k) : ctx->force_class;
-  if (cls == MF_CLASS_SMALL && k > mf::kSmallMaxK) return MF_BAD_ARG;
+  if (cls == MF_CLASS_SMALL && k > mf::small_max_k(dtype)) return MF_BAD_ARG;
   if (cls == MF_CLASS_MEDIUM && k > mf::kMediumMaxK) return MF_BAD_ARG;
   cudaError_t e;
   if (cls == MF_CLASS_SMALL) {

@@ -9,29 +9,7 @@ namespace mf {
 
 namespace {
 template <int DT, int K>
-cudaError_t launch_k(const Geom& g, cudaStream_t s) {
-  constexpr int kSmallThreads = SmallShape<DT, K>::T;
-  using C = SmallCfg<DT, K, kSmallThreads>;
-  auto kern = mf_small_kernel<DT, K, kSmallThreads>;
-  static int resident = 0;  // CTAs per SM (per process; the attribute is idempotent)
-  static int sms = 0;
-  if (!resident) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, kSmallThreads, C::smem);
-    if (e != cudaSuccess) return e;
-    if (resident < 1) resident = 1;
-  }
-  const uint64_t tiles_per_row = (g.units + C::TU - 1) / C::TU;
-  const uint64_t total = tiles_per_row * g.rows;
-  // persistent grid: each CTA streams a contiguous range of tiles with a prefetch
-  const uint64_t ctas = std::min<uint64_t>(total, (uint64_t)sms * resident);
-  kern<<<(unsigned)ctas, kSmallThreads, C::smem, s>>>(g, tiles_per_row, total);
-  return cudaGetLastError();
-}
+cudaError_t launch_k(const Geom& g, cudaStream_t s) { return small_launch_k<DT, K>(g, s); }
 
 // ---- k = 3: direct selection ------------------------------------------------------------
 // With k = 3 the paper's blocks hold three samples and every window spans two blocks, so the
@@ -174,7 +152,9 @@ cudaError_t launch_dt(const Geom& g, cudaStream_t s) {
     MF_K(1) MF_K(3) MF_K(5) MF_K(7) MF_K(9) MF_K(11) MF_K(13) MF_K(15)
     MF_K(17) MF_K(19) MF_K(21) MF_K(23) MF_K(25) MF_K(27) MF_K(29) MF_K(31)
 #undef MF_K
-    default: return cudaErrorInvalidValue;
+    default:
+      if (sizeof(typename Traits<DT>::U) == 4 && g.k <= kSmallMaxK32) return launch_small_k63(DT, g, s);
+      return cudaErrorInvalidValue;
   }
 }
 }  // namespace

@@ -1,5 +1,5 @@
-// mf_small.cuh -- fused median filter for small windows (k <= 31): one thread per
-// block pair, both phases in one pass over HBM.
+// mf_small.cuh -- fused median filter for small windows (k <= 31, and k <= 47 for 32-bit
+// keys): one thread per block pair, both phases in one pass over HBM.
 //
 // Reference path replaced: median_filter<T> (filter.hpp:149-155) for k <= 31:
 //   pad_to_blocks (filter.hpp:28-36)   -> virtual padding in the tile loader
@@ -7,7 +7,7 @@
 //   run_postprocess (filter.hpp:64-106) + Block (block.hpp:24-146)
 //                                       -> the same Figure-7 state machine per pair,
 //                                          with each sorted list held as a k-bit
-//                                          live mask in one register.
+//                                          live mask in one register (64-bit past k = 31).
 // The Block's doubly linked list over sorted positions is the set of live sorted
 // positions, so prev[m]/next[m] are "highest live bit below m" / "lowest live bit
 // above m" (one clz/ffs each), and the stale-link undelete of dancing links is a
@@ -45,7 +45,15 @@ template <int DT, int K> struct SmallShape {
 #ifndef MF_SMALL_UPT_K3
 #define MF_SMALL_UPT_K3 4
 #endif
-  static constexpr int T = wide ? 128 : (K <= 5 ? MF_SMALL_T_K3 : K <= 7 ? 512 : K <= 23 ? 256 : MF_SMALL_T_K31);
+#ifndef MF_SMALL_T_K35
+#define MF_SMALL_T_K35 256  // k = 33, 35 (32-bit keys, 64-bit masks): measured 0.72 ms at k = 33 (128: 0.97)
+#endif
+#ifndef MF_SMALL_T_K47
+#define MF_SMALL_T_K47 128  // k = 37..47: measured 0.96 / 0.98 ms at k = 37 / 41 (256: 1.05 / 1.45)
+#endif
+  static constexpr int T = wide ? 128
+                                : (K <= 5 ? MF_SMALL_T_K3 : K <= 7 ? 512 : K <= 23 ? 256 : K <= 31 ? MF_SMALL_T_K31
+                                   : K <= 35 ? MF_SMALL_T_K35 : MF_SMALL_T_K47);
   static constexpr int UPT = wide ? (K <= 7 ? 4 : K <= 15 ? 2 : 1)
                                   : (K <= 5 ? MF_SMALL_UPT_K3 : K <= 11 ? 2 : K <= 23 ? 1 : MF_SMALL_UPT_K31);
 };
@@ -68,20 +76,28 @@ struct SmallCfg {
 };
 
 // Live masks carry a sentinel bit at position K (the reference's list node k,
-// block.hpp:21-24), so "next live" always exists and needs no branch.
-__device__ __forceinline__ uint32_t live_next(uint32_t mask, uint32_t r) {
+// block.hpp:21-24), so "next live" always exists and needs no branch.  K <= 31 uses 32-bit
+// masks, 33 <= K <= 63 64-bit ones.
+__device__ __forceinline__ uint32_t ffs_m(uint32_t m) { return (uint32_t)__ffs(m); }
+__device__ __forceinline__ uint32_t ffs_m(uint64_t m) { return (uint32_t)__ffsll((long long)m); }
+__device__ __forceinline__ uint32_t top_m(uint32_t m) { return 31u - (uint32_t)__clz(m); }
+__device__ __forceinline__ uint32_t top_m(uint64_t m) { return 63u - (uint32_t)__clzll((long long)m); }
+template <typename M>
+__device__ __forceinline__ uint32_t live_next(M mask, uint32_t r) {
   // lowest live position > r (r < K): the sentinel K when none
-  return r + (uint32_t)__ffs(mask >> (r + 1));
+  return r + ffs_m((M)(mask >> (r + 1)));
 }
-__device__ __forceinline__ uint32_t live_prev(uint32_t mask, uint32_t m, uint32_t K) {
-  // highest live position < m (m <= K <= 31), or K (the list head/tail node)
-  const uint32_t lo = mask & ((1u << m) - 1u);
-  return sel(lo != 0, 31u - (uint32_t)__clz(lo), K);
+template <typename M>
+__device__ __forceinline__ uint32_t live_prev(M mask, uint32_t m, uint32_t K) {
+  // highest live position < m (m <= K), or K (the list head/tail node)
+  const M lo = mask & (((M)1 << m) - (M)1);
+  return sel(lo != 0, top_m(lo), K);
 }
-__device__ __forceinline__ uint32_t live_succ(uint32_t mask, uint32_t m, uint32_t K) {
+template <typename M>
+__device__ __forceinline__ uint32_t live_succ(M mask, uint32_t m, uint32_t K) {
   // next[m] of the reference list: lowest live > m, or the list head when m = k
   const uint32_t nx = live_next(mask, m < K ? m : K - 1);
-  return sel(m == K, (uint32_t)__ffs(mask) - 1, nx);
+  return sel(m == K, ffs_m(mask) - 1, nx);
 }
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
@@ -188,10 +204,12 @@ __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_
       const uint8_t* rA = srank + c;
       const uint8_t* rB = srank + c + 1;
       constexpr uint32_t KK = K;
-      constexpr uint32_t SENT = 1u << K;
-      uint32_t maskA = SENT | (SENT - 1u);  // construct: all live, s = h, m = pi[h] (block.hpp:47-49)
+      using M = std::conditional_t<(K < 32), uint32_t, uint64_t>;
+      constexpr M SENT = (M)1 << K;
+      M maskA = SENT | (SENT - 1u);  // construct: all live, s = h, m = pi[h] (block.hpp:47-49)
       uint32_t mA = H, sA = H;
-      uint32_t maskB = SENT, mB = K, sB = 0;  // unwind: empty, m = k, s = 0 (block.hpp:62-63)
+      M maskB = SENT;
+      uint32_t mB = K, sB = 0;  // unwind: empty, m = k, s = 0 (block.hpp:62-63)
       U keyA = kA[H * SC], keyB = UMax<U>::v;
       ost[c * K] = keyA;                      // Peek of the constructed block (filter.hpp:81-82)
 #pragma unroll
@@ -199,14 +217,14 @@ __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_
         const uint32_t ra = rA[(i - 1) * SC];
         const uint32_t rb = rB[(i - 1) * SC];
         // Delete(A, i-1): block.hpp:71-87
-        maskA &= ~(1u << ra);
+        maskA &= ~((M)1 << ra);
         const bool belowA = ra < mA;
         const uint32_t m1 = sel(ra == mA, live_next(maskA, ra), mA);
         const uint32_t pv = live_prev(maskA, m1, KK);
         mA = sel(!belowA && sA > 0, pv, m1);
         sA -= (belowA || sA > 0) ? 1u : 0u;
         // Undelete(B, i-1): block.hpp:89-98
-        maskB |= 1u << rb;
+        maskB |= (M)1 << rb;
         mB = sel(rb < mB, live_prev(maskB, mB, KK), mB);
         // Balance: filter.hpp:90-95 (ties go to A; the sentinel is never smaller)
         keyA = sel(mA == KK, UMax<U>::v, kA[min(mA, KK - 1) * SC]);
@@ -257,6 +275,32 @@ __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_
     row = nrow;
     tr = ntr;
   }
+}
+
+// Launch the small kernel for one (dtype, K): persistent grid over the row-major tiles.
+template <int DT, int K>
+cudaError_t small_launch_k(const Geom& g, cudaStream_t s) {
+  constexpr int kSmallThreads = SmallShape<DT, K>::T;
+  using C = SmallCfg<DT, K, kSmallThreads>;
+  auto kern = mf_small_kernel<DT, K, kSmallThreads>;
+  static int resident = 0;  // CTAs per SM (per process; the attribute is idempotent)
+  static int sms = 0;
+  if (!resident) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, kSmallThreads, C::smem);
+    if (e != cudaSuccess) return e;
+    if (resident < 1) resident = 1;
+  }
+  const uint64_t tiles_per_row = (g.units + C::TU - 1) / C::TU;
+  const uint64_t total = tiles_per_row * g.rows;
+  // persistent grid: each CTA streams a contiguous range of tiles with a prefetch
+  const uint64_t ctas = total < (uint64_t)sms * resident ? total : (uint64_t)sms * resident;
+  kern<<<(unsigned)ctas, kSmallThreads, C::smem, s>>>(g, tiles_per_row, total);
+  return cudaGetLastError();
 }
 
 }  // namespace mf

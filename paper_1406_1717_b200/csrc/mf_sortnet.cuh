@@ -12,6 +12,7 @@
 // registers with every index static.
 #pragma once
 #include <cstdint>
+#include <utility>
 
 #include "mf_common.cuh"
 
@@ -19,8 +20,8 @@ namespace mf {
 
 struct NetList {
   int n;
-  uint8_t a[512];
-  uint8_t b[512];
+  uint8_t a[1024];  // K <= 63: at most 543 comparators
+  uint8_t b[1024];
 };
 
 constexpr NetList make_oem(int K) {
@@ -206,20 +207,18 @@ __device__ __forceinline__ KElem64 ldg_elem(const KElem64* p) {
   return r;
 }
 
-template <int K, int I, typename E>
-__device__ __forceinline__ void net_apply(E* v) {
-  if constexpr (I < OEM<K>::net.n) {
-    constexpr int a = OEM<K>::net.a[I];
-    constexpr int b = OEM<K>::net.b[I];
-    E::cswap(v[a], v[b]);
-    net_apply<K, I + 1>(v);
-  }
+template <int K, int I> struct NetPair {
+  static constexpr int a = OEM<K>::net.a[I], b = OEM<K>::net.b[I];
+};
+template <int K, typename E, int... I>
+__device__ __forceinline__ void net_apply(E* v, std::integer_sequence<int, I...>) {
+  (E::cswap(v[NetPair<K, I>::a], v[NetPair<K, I>::b]), ...);  // every index a constant
 }
 
 // Sort K register-resident elements (static indices only).
 template <int K, typename E>
 __device__ __forceinline__ void sort_regs(E (&v)[K]) {
-  if constexpr (K > 1) net_apply<K, 0>(v);
+  if constexpr (K > 1) net_apply<K>(v, std::make_integer_sequence<int, OEM<K>::net.n>{});
 }
 
 }  // namespace mf
