@@ -25,8 +25,12 @@ template <int DT, int R> struct WarpsFor {
 #ifndef MF_W_R4_WIDE
 #define MF_W_R4_WIDE 4  // ... for R <= 4 and 64-bit keys (config 1, f64 k = 101: 0.0646 -> 0.0600 ms)
 #endif
+#ifndef MF_W_R2
+#define MF_W_R2 2  // ... for R = 2 and 32-bit keys, k = 49..63 (8 teams: k = 49 1.71 ms, 2 teams: 1.64 ms)
+#endif
   static constexpr int value =
-      R >= 32 ? MF_W_R32 : (R >= 16 ? MF_W_R16 : R >= 8 ? MF_W_R8 : (wide ? MF_W_R4_WIDE : MF_W_R4));
+      R >= 32 ? MF_W_R32
+              : (R >= 16 ? MF_W_R16 : R >= 8 ? MF_W_R8 : (wide ? MF_W_R4_WIDE : R == 2 ? MF_W_R2 : MF_W_R4));
 };
 
 template <int DT, int R>
