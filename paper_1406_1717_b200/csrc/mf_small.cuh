@@ -48,12 +48,19 @@ template <int DT, int K> struct SmallShape {
 #ifndef MF_SMALL_T_K35
 #define MF_SMALL_T_K35 256  // k = 33, 35 (32-bit keys, 64-bit masks): measured 0.72 ms at k = 33 (128: 0.97)
 #endif
+#ifndef MF_SMALL_T_K41
+#define MF_SMALL_T_K41 128  // k = 37..41: measured 0.96 / 0.98 ms at k = 37 / 41 (256: 1.05 / 1.45)
+#endif
+#ifndef MF_SMALL_T_K45
+#define MF_SMALL_T_K45 64   // k = 43, 45: 1.20 ms at k = 45 (128: 1.43; smaller tiles fit more CTAs)
+#endif
 #ifndef MF_SMALL_T_K47
-#define MF_SMALL_T_K47 128  // k = 37..47: measured 0.96 / 0.98 ms at k = 37 / 41 (256: 1.05 / 1.45)
+#define MF_SMALL_T_K47 96   // k = 47: 1.30 ms (128: 1.44, 64: 1.44)
 #endif
   static constexpr int T = wide ? 128
                                 : (K <= 5 ? MF_SMALL_T_K3 : K <= 7 ? 512 : K <= 23 ? 256 : K <= 31 ? MF_SMALL_T_K31
-                                   : K <= 35 ? MF_SMALL_T_K35 : MF_SMALL_T_K47);
+                                   : K <= 35 ? MF_SMALL_T_K35 : K <= 41 ? MF_SMALL_T_K41
+                                   : K <= 45 ? MF_SMALL_T_K45 : MF_SMALL_T_K47);
   static constexpr int UPT = wide ? (K <= 7 ? 4 : K <= 15 ? 2 : 1)
                                   : (K <= 5 ? MF_SMALL_UPT_K3 : K <= 11 ? 2 : K <= 23 ? 1 : MF_SMALL_UPT_K31);
 };
