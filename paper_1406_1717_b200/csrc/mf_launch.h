@@ -10,14 +10,17 @@ namespace mf {
 
 // Largest k each fused class handles (per key width).
 constexpr uint32_t kSmallMaxK = 31;        // 64-bit keys
-constexpr uint32_t kSmallMaxK32 = 47;      // 32-bit keys (64-bit live masks past 31; the medium
+#ifndef MF_SMALL_MAXK32
+#define MF_SMALL_MAXK32 53
+#endif
+constexpr uint32_t kSmallMaxK32 = MF_SMALL_MAXK32;      // 32-bit keys (64-bit live masks past 31; the medium
                                            // kernel measured faster from k = 55 on)
 inline uint32_t small_max_k(int dt) { return (dt == DT_I32 || dt == DT_F32) ? kSmallMaxK32 : kSmallMaxK; }
 constexpr uint32_t kMediumMaxK = 1023;
 
 // Fused small-k kernel (k odd, k <= small_max_k(dt)).
 cudaError_t launch_small(int dt, const Geom& g, cudaStream_t s, uint64_t* launches);
-// ... its 33 <= k <= 47 instantiations (32-bit keys; mf_small63.cu)
+// ... its 33 <= k <= 53 instantiations (32-bit keys; mf_small63.cu)
 cudaError_t launch_small_k63(int dt, const Geom& g, cudaStream_t s);
 // Fused medium-k kernel (k <= 1023).
 cudaError_t launch_medium(int dt, const Geom& g, cudaStream_t s, uint64_t* launches);

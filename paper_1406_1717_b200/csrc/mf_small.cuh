@@ -1,4 +1,4 @@
-// mf_small.cuh -- fused median filter for small windows (k <= 31, and k <= 47 for 32-bit
+// mf_small.cuh -- fused median filter for small windows (k <= 31, and k <= 53 for 32-bit
 // keys): one thread per block pair, both phases in one pass over HBM.
 //
 // Reference path replaced: median_filter<T> (filter.hpp:149-155) for k <= 31:
@@ -54,13 +54,16 @@ template <int DT, int K> struct SmallShape {
 #ifndef MF_SMALL_T_K45
 #define MF_SMALL_T_K45 64   // k = 43, 45: 1.20 ms at k = 45 (128: 1.43; smaller tiles fit more CTAs)
 #endif
+#ifndef MF_SMALL_T_K53
+#define MF_SMALL_T_K53 96   // k = 49..53: 1.30 / 1.28 / 1.30 ms (64: 1.45; the medium kernel: 1.64 / 1.57 / 1.51)
+#endif
 #ifndef MF_SMALL_T_K47
 #define MF_SMALL_T_K47 96   // k = 47: 1.30 ms (128: 1.44, 64: 1.44)
 #endif
   static constexpr int T = wide ? 128
                                 : (K <= 5 ? MF_SMALL_T_K3 : K <= 7 ? 512 : K <= 23 ? 256 : K <= 31 ? MF_SMALL_T_K31
                                    : K <= 35 ? MF_SMALL_T_K35 : K <= 41 ? MF_SMALL_T_K41
-                                   : K <= 45 ? MF_SMALL_T_K45 : MF_SMALL_T_K47);
+                                   : K <= 45 ? MF_SMALL_T_K45 : K <= 47 ? MF_SMALL_T_K47 : MF_SMALL_T_K53);
   static constexpr int UPT = wide ? (K <= 7 ? 4 : K <= 15 ? 2 : 1)
                                   : (K <= 5 ? MF_SMALL_UPT_K3 : K <= 11 ? 2 : K <= 23 ? 1 : MF_SMALL_UPT_K31);
 };
