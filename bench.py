@@ -117,32 +117,67 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def make_input(cfg, rank, world, k_max, device):
-    """This rank's input slice of the global signal (device resident), plus shard info."""
+def input_range(cfg, rank, world):
+    """[begin, end) of the global signal this rank needs: the union over every k of its
+    halo'd shard (paper_1406_1717_b200.shard.input_union).  Pure arithmetic, CPU-tested."""
+    from paper_1406_1717_b200.shard import input_union
+    dtype, n, ks, gen, seed, rows = CONFIGS[cfg]
+    return input_union(n * world, ks, world, rank)
+
+
+def make_input(cfg, rank, world, device):
+    """This rank's input slice of the global signal (device resident) and its begin."""
     import torch
     import paper_1406_1717_b200 as mf
     dtype, n, ks, gen, seed, rows = CONFIGS[cfg]
     if rows > 1:   # batched rows: shard whole rows, global row r = stream offset r*n
         r0, r1 = mf.shard_rows(rows * world, world)[rank]
         x = mf.generate_device(gen, seed, (r1 - r0) * n, offset=r0 * n, device=device, mod=16)
-        return x.view(r1 - r0, n)
-    n_global = n * world
-    # the union of the shards for every k: take the widest halo
-    sh = mf.shard_outputs(n_global, min(ks), world)[rank]
-    begin, end = sh.in_begin, min(n_global, sh.in_end + k_max)
+        return x.view(r1 - r0, n), r0
+    begin, end = input_range(cfg, rank, world)
     if gen == "trend_f64":
-        full = mf.generate_trend_f64(seed, n_global)
+        full = mf.generate_trend_f64(seed, end)
         return torch.from_numpy(full[begin:end]).to(f"cuda:{device}"), begin
     return mf.generate_device(gen, seed, end - begin, offset=begin, device=device), begin
 
 
 def shard_views(cfg, x, begin, rank, world, k):
-    """(input view, n_out) of this rank's shard for window k."""
-    import paper_1406_1717_b200 as mf
+    """(input view, n_out) of this rank's shard for window k; the view always holds the
+    shard's n_in samples (shard_view raises otherwise)."""
+    from paper_1406_1717_b200.shard import shard_outputs, shard_view
     dtype, n, ks, gen, seed, rows = CONFIGS[cfg]
-    sh = mf.shard_outputs(n * world, k, world)[rank]
-    a = sh.in_begin - begin
-    return x[a:a + sh.n_in], sh.n_out
+    sh = shard_outputs(n * world, k, world)[rank]
+    return shard_view(x, begin, sh), sh.n_out
+
+
+def golden(cfg, k):
+    """Reference fold_checksum of the config's full output (tests/golden/configs.json,
+    produced by the reference itself)."""
+    p = os.path.join(ROOT, "tests", "golden", "configs.json")
+    if not os.path.exists(p):
+        return None
+    g = json.load(open(p))
+    return g.get(f"{cfg}_k{k}", g.get(cfg))
+
+
+def output_checksums(cfg, jobs, outs, world, rank, dist):
+    """fold_checksum (io.hpp:17-28) of every k's global output, chained over ranks in
+    rank order, and (N = 1) the reference's golden value for the same config."""
+    import paper_1406_1717_b200 as mf
+    from paper_1406_1717_b200.shard import chained_fold_checksum
+    res = {}
+    for k, xv, nout in jobs:
+        y = outs[k]
+        y = (y[:, :xv.shape[1] - k + 1] if y.dim() == 2 else y[:nout]).contiguous().cpu().numpy()
+        h = chained_fold_checksum(y, world, rank, dist=dist if world > 1 else None, fold=mf.fold_checksum)
+        if rank == 0:
+            ent = {"out_cksum": str(h)}
+            gd = golden(cfg, k)
+            if world == 1 and gd is not None and gd.get("k") == k:
+                ent["golden"] = str(gd["out_cksum"])
+                ent["match"] = h == gd["out_cksum"]
+            res[str(k)] = ent
+    return res
 
 
 def run_ours(args):
@@ -169,11 +204,11 @@ def run_ours(args):
 
     with torch.cuda.stream(stream):
         if rows > 1:
-            x = make_input(cfg, rank, world, max(ks), local)
+            x, _r0 = make_input(cfg, rank, world, local)
             jobs = [(k, x, x.shape[0] * (n - k + 1)) for k in ks]
             outs = {k: torch.empty((x.shape[0], n - k + 1), dtype=x.dtype, device=x.device) for k in ks}
         else:
-            x, begin = make_input(cfg, rank, world, max(ks), local)
+            x, begin = make_input(cfg, rank, world, local)
             jobs = []
             outs = {}
             for k in ks:
@@ -242,10 +277,37 @@ def run_ours(args):
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(f"{cfg}_k{kdom}")
 
-    # end to end through the public host API (pinned host buffers, H2D + D2H timed)
+    # fold_checksum of every k's global output (chained over ranks), against the golden
+    checks = None
+    if not args.no_check:
+        checks = output_checksums(cfg, jobs, outs, world, rank, dist)
+
+    # optional final gather of the dominant k's outputs onto rank 0 (device gather over
+    # NCCL; reported separately, outside the timed region)
+    gather = None
+    if world > 1 and not args.no_gather:
+        from paper_1406_1717_b200.shard import gather_outputs_device
+        kk0, xv0, nout0 = [j for j in jobs if j[0] == max(per_k_ms, key=per_k_ms.get)][0]
+        part = outs[kk0][:nout0] if rows == 1 else outs[kk0]
+        if backend != "nccl":
+            part = part.cpu()
+        dist.barrier()
+        g0 = time.perf_counter()
+        full = gather_outputs_device(part, world, rank, dist=dist)
+        if full is not None and full.is_cuda:
+            torch.cuda.synchronize()
+        gms = (time.perf_counter() - g0) * 1e3
+        if rank == 0:
+            gather = {"k": kk0, "ms": gms, "bytes": int(full.numel() * full.element_size()),
+                      "how": "torch.distributed.gather of padded device tensors (NCCL send/recv)" if backend == "nccl"
+                             else "torch.distributed.gather (gloo, host tensors)"}
+        del full
+
+    # end to end through the public host API (host buffers, H2D + D2H timed), every rank
+    # on its own shard, max over ranks
     e2e = None
-    if rank == 0 and world == 1 and not args.no_e2e:
-        e2e = run_e2e(cfg, jobs, args, width)
+    if not args.no_e2e:
+        e2e = run_e2e(cfg, jobs, args, width, world, dist, red_dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -272,6 +334,8 @@ def run_ours(args):
                        "per_k_ms": {str(k): per_k_ms[k] for k in ks},
                        "per_k_samples_per_s": {str(k): [j[2] for j in jobs if j[0] == k][0] * world / (per_k_ms[k] / 1e3)
                                                for k in ks}},
+            "checksums": checks,
+            "gather": gather,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel_k": kdom,
                          "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src},
@@ -285,45 +349,68 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_e2e(cfg, jobs, args, width):
-    """Same metric through the host-buffer C ABI (mf_median_filter / _rows): every step
-    copies the input H2D from pinned memory and the medians D2H inside the timed region."""
+def run_e2e(cfg, jobs, args, width, world=1, dist=None, red_dev="cpu"):
+    """Same metric through the host-buffer C ABI (mf_median_filter / _rows, the literal
+    drop-in): every step copies the input H2D and the medians D2H inside the timed region.
+    Measured twice: from pinned host buffers (the headline) and from pageable ones (what a
+    std::vector caller of gpu.hpp hands over).  Every rank runs its own shard; the time is
+    the max over ranks and the value counts all ranks' outputs."""
     import torch
     import paper_1406_1717_b200 as mf
-    ctx = mf.Context.get(torch.cuda.current_device())
-    hx = {}
-    hy = {}
-    for k, xv, nout in jobs:
-        hx[k] = xv.cpu().pin_memory().numpy()
-        shape = (xv.shape[0], xv.shape[1] - k + 1) if xv.dim() == 2 else (max(nout, 1),)
-        hy[k] = torch.empty(shape, dtype=xv.dtype).pin_memory().numpy()
     import ctypes as C
     from paper_1406_1717_b200 import _native as N
     from paper_1406_1717_b200.filter import _DTYPES, _check
+    ctx = mf.Context.get(torch.cuda.current_device())
     L = N.lib()
-
-    def one(k):
-        x, y = hx[k], hy[k]
-        if x.ndim == 2:
-            _check(L.mf_median_filter_rows(ctx.handle, _DTYPES[x.dtype], x.ctypes.data, x.shape[0], x.shape[1],
-                                           x.shape[1], k, y.ctypes.data, y.shape[1]))
-        else:
-            ylen = C.c_size_t()
-            _check(L.mf_median_filter(ctx.handle, _DTYPES[x.dtype], x.ctypes.data, x.size, k, y.ctypes.data,
-                                      y.size, C.byref(ylen)))
     steps = max(1, min(args.steps, 5))
-    for k, _x, _n in jobs:
-        one(k)
-    t = time.perf_counter()
-    for _ in range(steps):
+    outputs = sum(n for _k, _x, n in jobs)
+    res = {}
+    for mode in ("pinned", "pageable"):
+        hx, hy = {}, {}
+        for k, xv, nout in jobs:
+            shape = (xv.shape[0], xv.shape[1] - k + 1) if xv.dim() == 2 else (max(nout, 1),)
+            if mode == "pinned":
+                hx[k] = xv.cpu().pin_memory().numpy()
+                hy[k] = torch.empty(shape, dtype=xv.dtype).pin_memory().numpy()
+            else:
+                hx[k] = xv.cpu().numpy().copy()
+                hy[k] = np.empty(shape, dtype=hx[k].dtype)
+
+        def one(k):
+            x, y = hx[k], hy[k]
+            if x.ndim == 2:
+                _check(L.mf_median_filter_rows(ctx.handle, _DTYPES[x.dtype], x.ctypes.data, x.shape[0], x.shape[1],
+                                               x.shape[1], k, y.ctypes.data, y.shape[1]))
+            else:
+                ylen = C.c_size_t()
+                _check(L.mf_median_filter(ctx.handle, _DTYPES[x.dtype], x.ctypes.data, x.size, k, y.ctypes.data,
+                                          y.size, C.byref(ylen)))
         for k, _x, _n in jobs:
             one(k)
-    dt = time.perf_counter() - t
-    outputs = sum(n for _k, _x, n in jobs)
-    return {"value": outputs * steps / dt, "unit": "samples/s",
-            "h2d_bytes_per_step": int(sum(hx[k].nbytes for k in hx)),
-            "d2h_bytes_per_step": int(sum(hy[k].nbytes for k in hy)),
-            "steps": steps, "api": "mf_median_filter (host buffers, pinned)"}
+        if world > 1:
+            dist.barrier()
+        t = time.perf_counter()
+        for _ in range(steps):
+            for k, _x, _n in jobs:
+                one(k)
+        dt = time.perf_counter() - t
+        tot = outputs
+        if world > 1:
+            tt = torch.tensor([dt], dtype=torch.float64, device=red_dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt.item())
+            o = torch.tensor([float(outputs)], dtype=torch.float64, device=red_dev)
+            dist.all_reduce(o, op=dist.ReduceOp.SUM)
+            tot = float(o.item())
+        res[mode] = {"value": tot * steps / dt, "steps": steps,
+                     "h2d_bytes_per_step": int(sum(hx[k].nbytes for k in hx)),
+                     "d2h_bytes_per_step": int(sum(hy[k].nbytes for k in hy))}
+        del hx, hy
+    p = res["pinned"]
+    return {"value": p["value"], "unit": "samples/s", "h2d_bytes_per_step": p["h2d_bytes_per_step"],
+            "d2h_bytes_per_step": p["d2h_bytes_per_step"], "steps": p["steps"],
+            "api": "mf_median_filter / mf_median_filter_rows (host buffers, pinned); per-rank bytes",
+            "pageable_value": res["pageable"]["value"]}
 
 
 def _ref_lib():
@@ -349,44 +436,74 @@ def _host_input(cfg, n_sample):
     return o.trend_f64(seed, n_sample)
 
 
-def _time_ref(lib, kind, cfg, x, threads):
+def _keyed_input(lib, kind, cfg, n_sample):
+    """The config's input on the host, already key-mapped (floats -> signed totalOrder
+    keys) and in the width the reference instantiation takes: the key
+    map is not part of the timed reference path."""
     from oracle_lib import keymap
+    dtype, n, ks, gen, seed, rows = CONFIGS[cfg]
+    kx = np.ascontiguousarray(keymap(_host_input(cfg, n_sample)))
+    if kind != "reference":
+        kx = kx.astype(np.int64)
+    return kx.reshape(-1, n) if rows > 1 else kx
+
+
+def _time_ref(lib, kind, cfg, kx, threads):
+    """One pass of the reference over the keyed input (every k of the config): the
+    reference's median_filter<T> halo-sharded over `threads` host threads, or rows over
+    threads.  Returns (outputs, seconds)."""
     dtype, n, ks, gen, seed, rows = CONFIGS[cfg]
     outs = 0
     t = time.perf_counter()
     for k in ks:
         if rows > 1:
-            rr = x.size // n
-            y = lib.median_filter_rows(x.reshape(rr, n), k, threads) if kind == "reference" else None
-            if y is None:
-                for r in range(rr):
-                    lib.median_filter_threads(x[r * n:(r + 1) * n].astype(np.int64), k, threads)
-            outs += rr * (n - k + 1)
-        else:
-            kx = keymap(x)
             if kind == "reference":
-                lib.median_filter_threads(kx, k, threads)
+                lib.median_filter_rows(kx, k, threads)
             else:
-                lib.median_filter_threads(kx.astype(np.int64), k, threads)
-            outs += x.size - k + 1
+                for r in range(kx.shape[0]):
+                    lib.median_filter_threads(kx[r], k, threads)
+            outs += kx.shape[0] * (n - k + 1)
+        else:
+            lib.median_filter_threads(kx, k, threads)
+            outs += kx.size - k + 1
     return outs, time.perf_counter() - t
 
 
-def cpu_baseline(cfg, args):
-    """The reference CPU path on this host, single core, on a bounded sample."""
-    lib, kind = _ref_lib()
+def _sample(cfg, cap):
     dtype, n, ks, gen, seed, rows = CONFIGS[cfg]
-    sample = min(n * rows, args.cpu_sample)
+    sample = min(n * rows, cap)
     if rows > 1:
         sample = max(n, sample // n * n)
-    x = _host_input(cfg, sample)
-    outs, dt = _time_ref(lib, kind, cfg, x, 1)
-    return {"value": outs / dt, "unit": "samples/s", "cores": 1, "kind": kind,
-            "sample": f"first {sample} samples of the {cfg} signal, every k of the config, 1 thread",
-            "seconds": dt}
+    return sample
+
+
+def _sample_text(cfg, sample, threads):
+    dtype, n, ks, gen, seed, rows = CONFIGS[cfg]
+    whole = "the whole" if sample >= n * rows else f"the first {sample} samples of the"
+    return (f"{whole} {cfg} signal ({sample} samples{f', {sample // n} rows' if rows > 1 else ''}), every k of "
+            f"the config, input key-mapped before timing, {'rows' if rows > 1 else 'halo-sharded'} over "
+            f"{threads} host threads")
+
+
+def cpu_baseline(cfg, args):
+    """The reference CPU path on this host (all threads) on a bounded sample of the same
+    workload: 1 warm-up, 3 repeats, median (bench.hpp:100-122)."""
+    lib, kind = _ref_lib()
+    threads = os.cpu_count() or 1
+    sample = _sample(cfg, args.cpu_sample)
+    kx = _keyed_input(lib, kind, cfg, sample)
+    _time_ref(lib, kind, cfg, kx, threads)
+    runs = [_time_ref(lib, kind, cfg, kx, threads) for _ in range(3)]
+    outs = runs[0][0]
+    dt = statistics.median(r[1] for r in runs)
+    return {"value": outs / dt, "unit": "samples/s", "cores": threads, "kind": kind,
+            "sample": _sample_text(cfg, sample, threads) + "; median of 3 after 1 warm-up", "seconds": dt}
 
 
 def run_reference(args):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref, the unmodified
+    headers) over every host thread, on the config's signal (c5: a 2^28-sample prefix),
+    W warm-up passes, K timed passes, median (bench.hpp:100-122)."""
     world, rank, local = dist_env()
     if rank != 0:
         return
@@ -394,20 +511,17 @@ def run_reference(args):
     cfg = args.config
     dtype, n, ks, gen, seed, rows = CONFIGS[cfg]
     threads = os.cpu_count() or 1
-    sample = min(n * rows, args.ref_sample)
-    if rows > 1:
-        sample = max(n, sample // n * n)
-    x = _host_input(cfg, sample)
+    sample = _sample(cfg, args.ref_sample)
+    kx = _keyed_input(lib, kind, cfg, sample)
     for _ in range(args.warmup):
-        _time_ref(lib, kind, cfg, x, threads)
-    tot_o, tot_t = 0, 0.0
+        _time_ref(lib, kind, cfg, kx, threads)
     times = []
+    outs = 0
     for _ in range(args.steps):
-        o, t = _time_ref(lib, kind, cfg, x, threads)
-        tot_o += o
-        tot_t += t
+        outs, t = _time_ref(lib, kind, cfg, kx, threads)
         times.append(t)
-    value = tot_o / tot_t
+    med = statistics.median(times)
+    value = outs / med
     line = {
         "impl": "reference",
         "metric": "median-filter output samples/sec",
@@ -416,16 +530,16 @@ def run_reference(args):
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": 1e3 * tot_t / args.steps,
+        "ms_per_step": 1e3 * med,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": {"float32": "f32", "float64": "f64", "int32": "i32"}[dtype],
         "data": "synthetic: SplitMix64 recipe of SURVEY.md §8(d), host generated",
-        "config": {"workload": WORKLOAD[cfg], "k": list(ks), "sample_samples": sample},
+        "config": {"workload": WORKLOAD[cfg], "k": list(ks), "sample_samples": sample,
+                   "same_as_gpu_config": sample >= n * rows, "timing": "median of K passes"},
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": kind,
-                         "sample": f"first {sample} samples of the {cfg} signal per step, every k, "
-                                   f"halo-sharded over {threads} threads"},
+                         "sample": _sample_text(cfg, sample, threads)},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -440,9 +554,17 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=1 << 23)
-    ap.add_argument("--ref-sample", type=int, default=1 << 24)
+    ap.add_argument("--no-check", action="store_true", help="skip the output fold_checksums")
+    ap.add_argument("--no-gather", action="store_true", help="skip the (untimed) final gather at N > 1")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 26)
+    ap.add_argument("--ref-sample", type=int, default=1 << 28)
+    ap.add_argument("--n-per-gpu", type=int, default=None,
+                    help="override the config's samples per GPU (per row for c3); tests and quick runs only")
     args = ap.parse_args()
+    if args.n_per_gpu:
+        dtype, n, ks, gen, seed, rows = CONFIGS[args.config]
+        CONFIGS[args.config] = (dtype, args.n_per_gpu, ks, gen, seed, rows)
+        WORKLOAD[args.config] += f" [n per GPU overridden to {args.n_per_gpu}]"
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
         args.warmup = 3

@@ -13,6 +13,7 @@
 #include <concepts>
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 #include <limits>
 #include <memory>
 #include <span>
@@ -33,15 +34,48 @@ inline void check(mf_status st) {
   throw std::runtime_error(std::string(mf_status_string(st)) + ": " + mf_error_message(st));
 }
 
+// Devices the calling thread's context spans: set_devices(), else the environment
+// variable MEDFILT_GPU_DEVICES ("0,1,2,3" or "all"), else device 0.
+inline std::vector<int> env_devices() {
+  std::vector<int> d;
+  const char* e = std::getenv("MEDFILT_GPU_DEVICES");
+  if (!e || !*e) return {0};
+  if (std::string(e) == "all") {
+    mf_context* probe = nullptr;
+    for (int i = 0; mf_context_create(i, &probe) == MF_OK; ++i) {
+      mf_context_destroy(probe);
+      d.push_back(i);
+    }
+    return d.empty() ? std::vector<int>{0} : d;
+  }
+  for (const char* p = e; *p;) {
+    char* end = nullptr;
+    const long v = std::strtol(p, &end, 10);
+    if (end == p) break;
+    d.push_back((int)v);
+    p = *end == ',' ? end + 1 : end;
+  }
+  return d.empty() ? std::vector<int>{0} : d;
+}
+
 // One context per host thread (contexts are not shared across threads).
+struct Holder {
+  mf_context* ctx = nullptr;
+  std::vector<int> devices = env_devices();
+  ~Holder() { mf_context_destroy(ctx); }
+};
+inline Holder& holder() {
+  thread_local Holder h;
+  return h;
+}
+
 inline mf_context* context() {
-  struct Holder {
-    mf_context* ctx = nullptr;
-    ~Holder() { mf_context_destroy(ctx); }
-  };
-  thread_local Holder holder;
-  if (!holder.ctx) check(mf_context_create(0, &holder.ctx));
-  return holder.ctx;
+  Holder& h = holder();
+  if (!h.ctx) {
+    if (h.devices.size() == 1) check(mf_context_create(h.devices[0], &h.ctx));
+    else check(mf_context_create_multi(h.devices.data(), (int)h.devices.size(), &h.ctx));
+  }
+  return h.ctx;
 }
 
 template <typename T> constexpr mf_dtype dtype_of();
@@ -63,6 +97,17 @@ std::vector<T> run(std::span<const T> x, std::size_t k) {
 }
 
 }  // namespace detail
+
+/// Devices the calling thread's median_filter calls use (SURVEY.md §8(b) "Multi-GPU entry:
+/// a device list").  With more than one device every call shards its signal (contiguous
+/// output ranges with a (k-1)-sample halo) or its rows across them; outputs are unchanged.
+inline void set_devices(std::vector<int> devices) {
+  if (devices.empty()) throw std::invalid_argument("device list must not be empty");
+  detail::Holder& h = detail::holder();
+  mf_context_destroy(h.ctx);
+  h.ctx = nullptr;
+  h.devices = std::move(devices);
+}
 
 /// median_filter<T> (filter.hpp:149-155) on the B200.
 template <std::signed_integral T>

@@ -64,6 +64,16 @@ int mf_kernel_class(mf_dtype dtype, size_t k);
 
 /* ---- context: device, stream and a grow-only device workspace (no per-call cudaMalloc) ---- */
 mf_status mf_context_create(int device, mf_context** out);
+/* Multi-device context over `ndev` CUDA devices (one sub-context each; a device may be
+ * listed twice, e.g. for tests).  The host entries (mf_median_filter, mf_median_filter_rows)
+ * shard their work across the devices, one host thread each: a single signal by contiguous
+ * output ranges with a (k-1)-sample input halo, a batch by whole row groups (SURVEY.md
+ * §8(e)); each device's D2H lands directly at its offset of the caller's output.  Outputs
+ * are identical to a single-device call.  Device-pointer entries reject a multi-device
+ * context with MF_BAD_ARG (a device pointer lives on one device). */
+mf_status mf_context_create_multi(const int* devices, int ndev, mf_context** out);
+/* Number of devices of ctx; writes up to `cap` device ids to `devices` (may be NULL). */
+int mf_context_devices(const mf_context* ctx, int* devices, int cap);
 void mf_context_destroy(mf_context* ctx);
 mf_status mf_context_set_option(mf_context* ctx, mf_option opt, long value);
 /* Number of kernels the last call on this context launched. */
@@ -77,7 +87,10 @@ mf_status mf_median_filter(mf_context* ctx, mf_dtype dtype, const void* x, size_
 
 /* ---- device entry: d_x / d_y are device pointers on ctx's device; stream-ordered on
  * `stream` (a cudaStream_t; NULL = the default stream, as in the CUDA runtime); returns
- * after enqueueing.  The host entries use the context's own stream. */
+ * after enqueueing.  The host entries use the context's own stream.  Calls on one context
+ * may be issued on different streams: the context's large-k workspace is ordered across
+ * them with an event, so such calls serialise on the device instead of sharing scratch.
+ * k > 2^31 - 65 (large class) returns MF_BAD_ARG. */
 mf_status mf_median_filter_device(mf_context* ctx, mf_dtype dtype, const void* d_x, size_t n, size_t k,
                                   void* d_y, void* stream);
 
@@ -105,6 +118,12 @@ enum { MF_GEN_UNIFORM_F32 = 0, MF_GEN_UNIFORM_F64 = 1, MF_GEN_MOD_I32 = 2 };
 /* Host generator of the config-4 signal x_i = i/n + 0.01*sqrt(-2 ln(1-u1))*cos(2 pi u2)
  * (libm-dependent, so generated on the host; SURVEY.md §8(c) pitfall). */
 void mf_generate_trend_f64_host(uint64_t seed, size_t n, double* out);
+
+/* fold_checksum (io.hpp:17-28) on the host: FNV-1a over the 8 bytes of each value (32-bit
+ * values sign-extended; float/double folded over their totalOrder keys).  Chainable:
+ * start from MF_FOLD_INIT, and fold(a ++ b) = mf_fold_checksum(dt, b, nb, fold(a)). */
+#define MF_FOLD_INIT 1469598103934665603ull
+uint64_t mf_fold_checksum(mf_dtype dtype, const void* values, size_t n, uint64_t state);
 
 #ifdef __cplusplus
 }

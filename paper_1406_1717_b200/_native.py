@@ -23,11 +23,12 @@ MF_GEN_UNIFORM_F32, MF_GEN_UNIFORM_F64, MF_GEN_MOD_I32 = 0, 1, 2
 # Every symbol include/medfilt_gpu.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "mf_status_string", "mf_error_message", "mf_window_spec", "mf_kernel_class",
-    "mf_context_create", "mf_context_destroy", "mf_context_set_option", "mf_context_last_launches",
+    "mf_context_create", "mf_context_create_multi", "mf_context_devices", "mf_context_destroy", "mf_context_set_option", "mf_context_last_launches",
     "mf_median_filter", "mf_median_filter_device", "mf_median_filter_rows",
     "mf_median_filter_rows_device", "mf_block_sort_device", "mf_generate_device",
-    "mf_generate_trend_f64_host",
+    "mf_generate_trend_f64_host", "mf_fold_checksum",
 )
+MF_FOLD_INIT = 1469598103934665603
 
 _lock = threading.Lock()
 _lib = None
@@ -56,6 +57,8 @@ def lib() -> C.CDLL:
         L.mf_window_spec.argtypes = [sz, sz, vp, vp, vp]
         L.mf_kernel_class.argtypes = [C.c_int, sz]
         L.mf_context_create.argtypes = [C.c_int, C.POINTER(vp)]
+        L.mf_context_create_multi.argtypes = [C.POINTER(C.c_int), C.c_int, C.POINTER(vp)]
+        L.mf_context_devices.argtypes = [vp, C.POINTER(C.c_int), C.c_int]
         L.mf_context_destroy.argtypes = [vp]
         L.mf_context_destroy.restype = None
         L.mf_context_set_option.argtypes = [vp, C.c_int, C.c_long]
@@ -69,6 +72,8 @@ def lib() -> C.CDLL:
         L.mf_generate_device.argtypes = [vp, C.c_int, u64, u64, u64, sz, vp, vp]
         L.mf_generate_trend_f64_host.argtypes = [u64, sz, vp]
         L.mf_generate_trend_f64_host.restype = None
+        L.mf_fold_checksum.argtypes = [C.c_int, vp, sz, u64]
+        L.mf_fold_checksum.restype = u64
         _lib = L
         return L
 

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../../include/medfilt_gpu.h"
@@ -27,6 +28,14 @@ struct mf_context {
   // host-entry pipeline: H2D / compute / D2H on three streams, up to 4 chunks in flight
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_in[16] = {}, ev_done[16] = {}, ev_out[16] = {};
+  // the workspace is shared by every call on this context, whatever stream it is issued on:
+  // each call that uses it records ws_ev, and the next one waits for it (stream order across
+  // streams, so concurrent large-k calls on two streams never overlap on ws)
+  cudaEvent_t ws_ev = nullptr;
+  bool ws_ev_recorded = false;
+  // multi-device context (mf_context_create_multi): one sub-context per device; the host
+  // entries shard their work over them.  Empty for a single-device context.
+  std::vector<mf_context*> subs;
   std::mutex mu;
 };
 
@@ -53,6 +62,19 @@ mf_status grow(void** p, size_t* cap, size_t need) {
   return MF_OK;
 }
 
+// Order a use of ctx->ws on stream s after the previous use (on whatever stream).
+mf_status ws_acquire(mf_context* ctx, cudaStream_t s) {
+  if (!ctx->ws_ev && cudaEventCreateWithFlags(&ctx->ws_ev, cudaEventDisableTiming) != cudaSuccess)
+    return MF_CUDA_ERROR;
+  if (ctx->ws_ev_recorded && cudaStreamWaitEvent(s, ctx->ws_ev, 0) != cudaSuccess) return MF_CUDA_ERROR;
+  return MF_OK;
+}
+cudaError_t ws_release(mf_context* ctx, cudaStream_t s) {
+  const cudaError_t e = cudaEventRecord(ctx->ws_ev, s);
+  ctx->ws_ev_recorded = e == cudaSuccess;
+  return e;
+}
+
 int class_for(mf_dtype dtype, size_t k) {
   if (k <= mf::small_max_k(dtype)) return MF_CLASS_SMALL;
   if (k <= mf::kMediumMaxK) return MF_CLASS_MEDIUM;
@@ -69,14 +91,16 @@ mf_status run_rows(mf_context* ctx, mf_dtype dtype, const void* d_x, size_t rows
   ctx->launches = 0;
   if (keep == 0 || rows == 0) return MF_OK;
   if (!d_x || !d_y || ld_x < n || ld_y < keep || rows > 0xFFFFFFFFull) return MF_BAD_ARG;
+  int cls = ctx->force_class == MF_CLASS_AUTO ? class_for(dtype, k) : ctx->force_class;
+  if (cls == MF_CLASS_SMALL && k > mf::small_max_k(dtype)) return MF_BAD_ARG;
+  if (cls == MF_CLASS_MEDIUM && k > mf::kMediumMaxK) return MF_BAD_ARG;
+  // the large-k pipeline packs 2k merged positions and a side flag into 32 bits
+  if (cls == MF_CLASS_LARGE && k > mf::kLargeMaxK) return MF_BAD_ARG;
   if (cudaSetDevice(ctx->device) != cudaSuccess) return MF_NO_DEVICE;
   mf::Geom g{};
   g.x = d_x; g.y = d_y; g.n = n; g.ld_x = ld_x; g.ld_y = ld_y;
   g.k = (uint32_t)k; g.h = (uint32_t)((k - 1) / 2);
   g.keep = keep; g.units = (keep + k - 1) / k; g.rows = (uint32_t)rows;
-  int cls = ctx->force_class == MF_CLASS_AUTO ? class_for(dtype, k) : ctx->force_class;
-  if (cls == MF_CLASS_SMALL && k > mf::small_max_k(dtype)) return MF_BAD_ARG;
-  if (cls == MF_CLASS_MEDIUM && k > mf::kMediumMaxK) return MF_BAD_ARG;
   cudaError_t e;
   if (cls == MF_CLASS_SMALL) {
     e = mf::launch_small(dtype, g, s, &ctx->launches);
@@ -85,6 +109,7 @@ mf_status run_rows(mf_context* ctx, mf_dtype dtype, const void* d_x, size_t rows
   } else {
     // the large-k kernels put rows on grid.y (<= 65535): run row groups
     const size_t w = dtype_size(dtype);
+    if ((st = ws_acquire(ctx, s)) != MF_OK) return st;
     e = cudaSuccess;
     for (size_t r0 = 0; r0 < rows && e == cudaSuccess; r0 += 65535) {
       mf::Geom gg = g;
@@ -96,6 +121,8 @@ mf_status run_rows(mf_context* ctx, mf_dtype dtype, const void* d_x, size_t rows
       if (st != MF_OK) return st;
       e = mf::run_large(dtype, gg, ctx->ws, ctx->ws_bytes, s, &ctx->launches);
     }
+    const cudaError_t er = ws_release(ctx, s);
+    if (e == cudaSuccess) e = er;
   }
   return from_cuda(e);
 }
@@ -167,11 +194,46 @@ mf_status mf_context_create(int device, mf_context** out) {
   return MF_OK;
 }
 
+mf_status mf_context_create_multi(const int* devices, int ndev, mf_context** out) {
+  if (!out) return MF_BAD_ARG;
+  *out = nullptr;
+  if (!devices || ndev < 1) return MF_BAD_ARG;
+  mf_context* ctx = new mf_context();
+  ctx->device = devices[0];
+  for (int i = 0; i < ndev; ++i) {
+    mf_context* sub = nullptr;
+    const mf_status st = mf_context_create(devices[i], &sub);
+    if (st != MF_OK) {
+      mf_context_destroy(ctx);
+      return st;
+    }
+    ctx->subs.push_back(sub);
+  }
+  *out = ctx;
+  return MF_OK;
+}
+
+int mf_context_devices(const mf_context* ctx, int* devices, int cap) {
+  if (!ctx) return 0;
+  if (ctx->subs.empty()) {
+    if (devices && cap > 0) devices[0] = ctx->device;
+    return 1;
+  }
+  for (int i = 0; i < (int)ctx->subs.size() && devices && i < cap; ++i) devices[i] = ctx->subs[i]->device;
+  return (int)ctx->subs.size();
+}
+
 void mf_context_destroy(mf_context* ctx) {
   if (!ctx) return;
+  if (!ctx->subs.empty()) {
+    for (mf_context* sub : ctx->subs) mf_context_destroy(sub);
+    delete ctx;
+    return;
+  }
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->ws_ev) cudaEventDestroy(ctx->ws_ev);
   if (ctx->io) cudaFree(ctx->io);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->s_h2d) cudaStreamSynchronize(ctx->s_h2d), cudaStreamDestroy(ctx->s_h2d);
@@ -186,6 +248,10 @@ void mf_context_destroy(mf_context* ctx) {
 
 mf_status mf_context_set_option(mf_context* ctx, mf_option opt, long value) {
   if (!ctx) return MF_BAD_ARG;
+  for (mf_context* sub : ctx->subs) {
+    const mf_status st = mf_context_set_option(sub, opt, value);
+    if (st != MF_OK) return st;
+  }
   if (opt == MF_OPT_FORCE_CLASS) {
     if (value < MF_CLASS_AUTO || value > MF_CLASS_LARGE) return MF_BAD_ARG;
     ctx->force_class = (int)value;
@@ -204,7 +270,7 @@ uint64_t mf_context_last_launches(const mf_context* ctx) { return ctx ? ctx->lau
 mf_status mf_median_filter_rows_device(mf_context* ctx, mf_dtype dtype, const void* d_x, size_t rows,
                                        size_t n, size_t ld_x, size_t k, void* d_y, size_t ld_y,
                                        void* stream) {
-  if (!ctx) return MF_BAD_ARG;
+  if (!ctx || !ctx->subs.empty()) return MF_BAD_ARG;  // device pointers live on one device
   std::lock_guard<std::mutex> lock(ctx->mu);
   return run_rows(ctx, dtype, d_x, rows, n, ld_x, k, d_y, ld_y, pick(ctx, stream));
 }
@@ -239,6 +305,53 @@ static std::vector<size_t> chunk_schedule(size_t total, size_t cmin, size_t cmax
   return out;
 }
 
+// Multi-device host entry: a single signal is cut into contiguous output
+// ranges [o_g, o_{g+1}) and device g filters x[o_g, o_{g+1}+k-1) -- a (k-1)-sample halo --
+// as an independent signal; a batch is cut into whole row groups.  Blocking never changes
+// an output (the reference's pair loop, filter.hpp:83-102, is
+// independent per pair), so the concatenation is the single-device result.  One host
+// thread per device runs the single-device pipeline, whose D2H writes straight into the
+// caller's output at offset o_g: the gather IS the D2H, no device-to-device exchange.
+// Caller holds ctx->mu.
+static mf_status multi_rows(mf_context* ctx, mf_dtype dtype, const void* x, size_t rows, size_t n, size_t ld_x,
+                            size_t k, void* y, size_t ld_y, size_t keep) {
+  struct Part { size_t xo, yo, rows, n, ld_x, ld_y; };
+  const size_t G = ctx->subs.size(), w = dtype_size(dtype);
+  std::vector<Part> parts;
+  if (rows > 1) {
+    const size_t use = std::min(G, rows);
+    for (size_t g = 0; g < use; ++g) {
+      const size_t r0 = rows * g / use, r1 = rows * (g + 1) / use;
+      parts.push_back({r0 * ld_x, r0 * ld_y, r1 - r0, n, ld_x, ld_y});
+    }
+  } else {
+    // shards of at least max(2^20, 16k) outputs: below that a device's launch and copy
+    // latency outweighs the work it takes over
+    const size_t min_out = std::max<size_t>(size_t(1) << 20, 16 * k);
+    const size_t use = std::max<size_t>(1, std::min(G, keep / min_out));
+    for (size_t g = 0; g < use; ++g) {
+      const size_t o0 = keep * g / use, o1 = keep * (g + 1) / use;
+      parts.push_back({o0, o0, 1, o1 - o0 + k - 1, o1 - o0 + k - 1, o1 - o0});
+    }
+  }
+  std::vector<mf_status> st(parts.size(), MF_OK);
+  auto run = [&](size_t i) {
+    const Part& p = parts[i];
+    st[i] = mf_median_filter_rows(ctx->subs[i], dtype, static_cast<const char*>(x) + p.xo * w, p.rows, p.n,
+                                  p.ld_x, k, static_cast<char*>(y) + p.yo * w, p.ld_y);
+  };
+  std::vector<std::thread> threads;
+  for (size_t i = 1; i < parts.size(); ++i) threads.emplace_back(run, i);
+  run(0);
+  for (auto& t : threads) t.join();
+  uint64_t launches = 0;
+  for (size_t i = 0; i < parts.size(); ++i) launches += ctx->subs[i]->launches;
+  ctx->launches = launches;
+  for (mf_status v : st)
+    if (v != MF_OK) return v;
+  return MF_OK;
+}
+
 // Host entry: the literal drop-in.  The signal (or batch) is cut into chunks of about
 // kChunkElems outputs -- contiguous output ranges with a (k-1)-sample input halo, or whole
 // rows -- and up to four chunks are kept in flight: H2D of chunk c+1, kernels of chunk c and D2H
@@ -255,6 +368,7 @@ mf_status mf_median_filter_rows(mf_context* ctx, mf_dtype dtype, const void* x, 
   ctx->launches = 0;
   if (keep == 0 || rows == 0) return MF_OK;
   if (!x || !y || ld_x < n || ld_y < keep) return MF_BAD_ARG;
+  if (!ctx->subs.empty()) return multi_rows(ctx, dtype, x, rows, n, ld_x, k, y, ld_y, keep);
   if (cudaSetDevice(ctx->device) != cudaSuccess) return MF_NO_DEVICE;
 #ifndef MF_PIPE_SLOTS
 #define MF_PIPE_SLOTS 4
@@ -360,7 +474,7 @@ mf_status mf_block_sort_device(mf_context* ctx, mf_dtype dtype, const void* d_x,
   size_t b = 0;
   mf_status st = mf_window_spec(n, k, nullptr, &b, nullptr);
   if (st != MF_OK) return st;
-  if (!dtype_ok(dtype) || !d_x || !d_perm) return MF_BAD_ARG;
+  if (!dtype_ok(dtype) || !d_x || !d_perm || !ctx->subs.empty() || k > mf::kLargeMaxK) return MF_BAD_ARG;
   std::lock_guard<std::mutex> lock(ctx->mu);
   ctx->launches = 0;
   if (cudaSetDevice(ctx->device) != cudaSuccess) return MF_NO_DEVICE;
@@ -370,12 +484,16 @@ mf_status mf_block_sort_device(mf_context* ctx, mf_dtype dtype, const void* d_x,
   g.keep = n >= k ? n - k + 1 : 0; g.units = b; g.rows = 1;
   st = grow(&ctx->ws, &ctx->ws_bytes, mf::block_sort_workspace_bytes(dtype, g, b));
   if (st != MF_OK) return st;
-  return from_cuda(mf::run_block_sort(dtype, g, b, ctx->ws, d_perm, pick(ctx, stream), &ctx->launches));
+  cudaStream_t s = pick(ctx, stream);
+  if ((st = ws_acquire(ctx, s)) != MF_OK) return st;
+  cudaError_t e = mf::run_block_sort(dtype, g, b, ctx->ws, d_perm, s, &ctx->launches);
+  const cudaError_t er = ws_release(ctx, s);
+  return from_cuda(e != cudaSuccess ? e : er);
 }
 
 mf_status mf_generate_device(mf_context* ctx, int kind, uint64_t seed, uint64_t mod, uint64_t offset, size_t n,
                              void* d_out, void* stream) {
-  if (!ctx || !d_out || kind < 0 || kind > 2 || (kind == 2 && mod == 0)) return MF_BAD_ARG;
+  if (!ctx || !ctx->subs.empty() || !d_out || kind < 0 || kind > 2 || (kind == 2 && mod == 0)) return MF_BAD_ARG;
   if (cudaSetDevice(ctx->device) != cudaSuccess) return MF_NO_DEVICE;
   return from_cuda(mf::launch_generate(kind, seed, mod, offset, n, d_out, pick(ctx, stream)));
 }

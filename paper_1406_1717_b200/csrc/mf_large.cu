@@ -43,35 +43,20 @@ LargeGeom plan(const Geom& g, uint64_t nb) {
   return L;
 }
 
-// per-process kernel attributes (idempotent)
+// kernel attributes, per device (kernel_setup)
 template <int DT>
 cudaError_t configure(const LargeGeom& L) {
   using U = typename Traits<DT>::U;
-  static bool done = false;
-  static size_t unit_merge_set = 0;
-  cudaError_t e = cudaSuccess;
-  if (!done) {
-    for (auto f : {ml_tile_sort<DT, true>, ml_tile_sort<DT, false>}) {
-      e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TileSort<U>::smem);
-      if (e != cudaSuccess) return e;
-    }
-    e = cudaFuncSetAttribute(ml_tile_radix<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TileRadix<U>::smem);
-    if (e != cudaSuccess) return e;
-    for (auto f : {ml_merge_pass<DT, true>, ml_merge_pass<DT, false>}) {
-      e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)merge_tile_smem<U>());
-      if (e != cudaSuccess) return e;
-    }
-    e = cudaFuncSetAttribute(ml_walk<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(sizeof(U) * 32 * 9 * (LNT / 32)));
-    if (e != cudaSuccess) return e;
-    done = true;
-  }
+  cudaError_t e;
+  for (auto f : {ml_tile_sort<DT, true>, ml_tile_sort<DT, false>})
+    if ((e = kernel_setup((const void*)f, TileSort<U>::smem, 0, nullptr)) != cudaSuccess) return e;
+  if ((e = kernel_setup((const void*)ml_tile_radix<DT>, TileRadix<U>::smem, 0, nullptr)) != cudaSuccess) return e;
+  for (auto f : {ml_merge_pass<DT, true>, ml_merge_pass<DT, false>})
+    if ((e = kernel_setup((const void*)f, merge_tile_smem<U>(), 0, nullptr)) != cudaSuccess) return e;
+  if ((e = kernel_setup((const void*)ml_walk<DT>, sizeof(U) * 32 * 9 * (LNT / 32), 0, nullptr)) != cudaSuccess)
+    return e;
   const size_t um = merge_tile_smem<U>() + sizeof(uint32_t) * 8 * L.C;
-  if (um > unit_merge_set) {
-    e = cudaFuncSetAttribute(ml_unit_merge<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)um);
-    if (e == cudaSuccess) unit_merge_set = um;
-  }
-  return e;
+  return kernel_setup((const void*)ml_unit_merge<DT>, um, 0, nullptr);
 }
 
 template <int DT>

@@ -8,6 +8,15 @@
 
 namespace mf {
 
+// Per-(device, kernel) launch setup (mf_setup.cu): applies the dynamic-smem opt-in on the
+// current device and returns its SM count and, for threads > 0, the resident CTAs per SM
+// at (threads, smem).  Thread-safe; cached per device.
+struct LaunchInfo {
+  int sms;
+  int resident;
+};
+cudaError_t kernel_setup(const void* func, size_t smem, int threads, LaunchInfo* out);
+
 // Largest k each fused class handles (per key width).
 constexpr uint32_t kSmallMaxK = 31;        // 64-bit keys
 #ifndef MF_SMALL_MAXK32
@@ -17,6 +26,10 @@ constexpr uint32_t kSmallMaxK32 = MF_SMALL_MAXK32;      // 32-bit keys (64-bit l
                                            // kernel measured faster from k = 55 on)
 inline uint32_t small_max_k(int dt) { return (dt == DT_I32 || dt == DT_F32) ? kSmallMaxK32 : kSmallMaxK; }
 constexpr uint32_t kMediumMaxK = 1023;
+// Largest k of the large-k pipeline: it packs 2k merged positions (padded to a multiple of
+// 32) into uint32 and a side flag into bit 31 of an in-block index.  The reference accepts
+// k <= 2^32 - 2 (core.hpp:68-69); larger windows are rejected with MF_BAD_ARG.
+constexpr uint64_t kLargeMaxK = (uint64_t(1) << 31) - 65;
 
 // Fused small-k kernel (k odd, k <= small_max_k(dt)).
 cudaError_t launch_small(int dt, const Geom& g, cudaStream_t s, uint64_t* launches);

@@ -39,18 +39,10 @@ cudaError_t launch_r(const Geom& g, cudaStream_t s) {
   constexpr int WP = R >= 32 ? 2 : 1;  // warps per block pair (team); k <= 511 measured faster with 1
   using C = MediumCfg<DT, R, W, WP>;
   auto kern = mf_medium_kernel<DT, R, W, WP>;
-  static int resident = 0;  // CTAs per SM (per process; the attribute is idempotent)
-  static int sms = 0;
-  if (!resident) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, 32 * W * WP, C::smem);
-    if (e != cudaSuccess) return e;
-    if (resident < 1) resident = 1;
-  }
+  LaunchInfo li;
+  cudaError_t e = kernel_setup((const void*)kern, C::smem, 32 * W * WP, &li);
+  if (e != cudaSuccess) return e;
+  const int sms = li.sms, resident = li.resident;
   const uint64_t tiles_per_row = (g.units + W - 1) / W;
   const uint64_t total = tiles_per_row * g.rows;
   // persistent grid: each CTA walks a contiguous range of tiles (ring-carried blocks)

@@ -126,12 +126,10 @@ template <int DT>
 cudaError_t launch_med3(const Geom& g, cudaStream_t s) {
   using T = typename Traits<DT>::T;
   constexpr uint64_t SPAN = (uint64_t)kMed3Threads * kMed3Q * (16 / sizeof(T));
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  LaunchInfo li;
+  cudaError_t e = kernel_setup((const void*)mf_med3_kernel<DT>, 0, 0, &li);
+  if (e != cudaSuccess) return e;
+  const int sms = li.sms;
   const uint64_t cpr = (g.keep + SPAN - 1) / SPAN;
   const bool vec = (reinterpret_cast<uintptr_t>(g.x) % 16 == 0) && (reinterpret_cast<uintptr_t>(g.y) % 16 == 0) &&
                    (g.ld_x * sizeof(T)) % 16 == 0 && (g.ld_y * sizeof(T)) % 16 == 0;

@@ -293,18 +293,10 @@ cudaError_t small_launch_k(const Geom& g, cudaStream_t s) {
   constexpr int kSmallThreads = SmallShape<DT, K>::T;
   using C = SmallCfg<DT, K, kSmallThreads>;
   auto kern = mf_small_kernel<DT, K, kSmallThreads>;
-  static int resident = 0;  // CTAs per SM (per process; the attribute is idempotent)
-  static int sms = 0;
-  if (!resident) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, kSmallThreads, C::smem);
-    if (e != cudaSuccess) return e;
-    if (resident < 1) resident = 1;
-  }
+  LaunchInfo li;
+  cudaError_t e = kernel_setup((const void*)kern, C::smem, kSmallThreads, &li);
+  if (e != cudaSuccess) return e;
+  const int sms = li.sms, resident = li.resident;
   const uint64_t tiles_per_row = (g.units + C::TU - 1) / C::TU;
   const uint64_t total = tiles_per_row * g.rows;
   // persistent grid: each CTA streams a contiguous range of tiles with a prefetch

@@ -71,15 +71,37 @@ def make_window_spec(n: int, k: int) -> WindowSpec:
 
 
 class Context:
-    """One mf_context (device, stream, grow-only workspace) per CUDA device."""
+    """One mf_context (device, stream, grow-only workspace) per CUDA device, or a
+    multi-device context (``Context.multi``) whose host-buffer calls shard over devices."""
 
     _cache: dict[int, "Context"] = {}
     _cache_lock = threading.Lock()
 
-    def __init__(self, device: int = 0):
-        self.device = device
+    def __init__(self, device: int = 0, *, devices=None):
         self._h = C.c_void_p()
-        _check(N.lib().mf_context_create(device, C.byref(self._h)))
+        if devices is None:
+            self.device = device
+            _check(N.lib().mf_context_create(device, C.byref(self._h)))
+        else:
+            devs = [int(d) for d in devices]
+            if not devs:
+                raise ValueError("device list must not be empty")
+            self.device = devs[0]
+            arr = (C.c_int * len(devs))(*devs)
+            _check(N.lib().mf_context_create_multi(arr, len(devs), C.byref(self._h)))
+
+    @classmethod
+    def multi(cls, devices) -> "Context":
+        """A context over several devices (mf_context_create_multi): median_filter and
+        median_filter_rows shard the signal (halo'd output ranges) or the rows across them."""
+        return cls(devices=devices)
+
+    @property
+    def devices(self) -> list[int]:
+        n = int(N.lib().mf_context_devices(self._h, None, 0))
+        arr = (C.c_int * n)()
+        N.lib().mf_context_devices(self._h, arr, n)
+        return list(arr)
 
     @classmethod
     def get(cls, device: int = 0) -> "Context":
@@ -235,6 +257,15 @@ def generate_device(kind: str, seed: int, n: int, *, offset: int = 0, device: in
     _check(N.lib().mf_generate_device(ctx.handle, code, seed, mod, offset, n, C.c_void_p(out.data_ptr()),
                                       _stream_of(out, stream)))
     return out
+
+
+def fold_checksum(values, state: int = N.MF_FOLD_INIT) -> int:
+    """fold_checksum (io.hpp:17-28) of a host array (floats over their totalOrder keys);
+    `state` chains: fold_checksum(b, fold_checksum(a)) == fold_checksum(concat(a, b))."""
+    v = np.ascontiguousarray(values)
+    if v.dtype not in _DTYPES:
+        raise TypeError(f"unsupported dtype {v.dtype}")
+    return int(N.lib().mf_fold_checksum(_DTYPES[v.dtype], v.ctypes.data, v.size, state))
 
 
 def generate_trend_f64(seed: int, n: int) -> np.ndarray:

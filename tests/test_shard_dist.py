@@ -35,6 +35,8 @@ def _worker(rank, world, port, k, n, q):
         shard = sh.shard_outputs(n, k, world)[rank]
         part = sh.run_shard(x, k, shard, orc.median_filter)    # rank-local filter, no exchange
         full = sh.gather_outputs([part], world, rank, dist=dist)
+        # fold_checksum of the global output, chained over ranks in rank order
+        cks = sh.chained_fold_checksum(part, world, rank, dist=dist)
         # rows: shard whole rows, gather
         xr = rng.integers(0, 16, size=(7, 3 * k + 5)).astype(np.int32)
         r0, r1 = sh.shard_rows(xr.shape[0], world)[rank]
@@ -45,25 +47,26 @@ def _worker(rank, world, port, k, n, q):
             want = orc.median_filter(x, k)
             want_rows = np.stack([orc.median_filter(xr[r], k) for r in range(xr.shape[0])])
             q.put((bool(np.array_equal(full.view(np.int32), want.view(np.int32))),
-                   bool(np.array_equal(rows_full, want_rows))))
+                   bool(np.array_equal(rows_full, want_rows)),
+                   cks == orc.fold_checksum(want)))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("k,n", [(3, 1000), (31, 5003), (255, 20000), (2049, 30011)])
-def test_sharded_equals_unsharded_gloo(k, n):
+@pytest.mark.parametrize("k,n,world", [(3, 1000, 2), (31, 5003, 2), (255, 20000, 2), (2049, 30011, 2),
+                                       (101, 7001, 3)])
+def test_sharded_equals_unsharded_gloo(k, n, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    world = 2
     procs = [ctx.Process(target=_worker, args=(r, world, port, k, n, q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    ok_signal, ok_rows = q.get(timeout=10)
-    assert ok_signal and ok_rows
+    ok_signal, ok_rows, ok_cks = q.get(timeout=10)
+    assert ok_signal and ok_rows and ok_cks
 
 
 def test_shard_plan_properties():
@@ -78,3 +81,18 @@ def test_shard_plan_properties():
             if s.n_out:
                 assert s.n_in == s.n_out + k - 1 and s.in_end <= n
     assert sh.shard_rows(10, 4) == [(0, 2), (2, 5), (5, 7), (7, 10)]
+
+
+def test_fold_checksum_matches_reference_and_chains():
+    """mf_fold_checksum (product library, host) == the oracle's fold_checksum (io.hpp:17-28)
+    for every dtype, and folding a continuation from a previous state equals folding the
+    concatenation (what the multi-rank bench relies on)."""
+    import paper_1406_1717_b200 as mf
+    from oracle_lib import Oracle
+    orc = Oracle()
+    rng = np.random.default_rng(5)
+    for dt in (np.int32, np.int64, np.float32, np.float64):
+        v = (rng.standard_normal(1001) * 1e3).astype(dt)
+        assert mf.fold_checksum(v) == orc.fold_checksum(v)
+        for cut in (0, 1, 500, 1001):
+            assert mf.fold_checksum(v[cut:], mf.fold_checksum(v[:cut])) == mf.fold_checksum(v)
