@@ -254,6 +254,10 @@ def run_ours(args):
     ms = t0.elapsed_time(t1)
     per_k_ms = {k: statistics.mean(a.elapsed_time(b) for a, b in ev[k]) for k in ks}
     outputs_rank = sum(nout for _k, _x, nout in jobs)
+    if world > 1:  # per-k kernel times: max over ranks, so every rank picks the same dominant k
+        pk = torch.tensor([per_k_ms[k] for k in ks], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(pk, op=dist.ReduceOp.MAX)
+        per_k_ms = {k: float(v) for k, v in zip(ks, pk.tolist())}
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -66,6 +66,8 @@ template <int DT, int K> struct SmallShape {
                                    : K <= 45 ? MF_SMALL_T_K45 : K <= 47 ? MF_SMALL_T_K47 : MF_SMALL_T_K53);
   static constexpr int UPT = wide ? (K <= 7 ? 4 : K <= 15 ? 2 : 1)
                                   : (K <= 5 ? MF_SMALL_UPT_K3 : K <= 11 ? 2 : K <= 23 ? 1 : MF_SMALL_UPT_K31);
+  // the cross-tile carry of the last block is spread over the first K threads (t < K)
+  static_assert(T >= K, "small-kernel CTA must have at least K threads");
 };
 
 template <int DT, int K, int T>
