@@ -6,14 +6,96 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <thread>
 #include <vector>
 
 #include "../../include/medfilt_gpu.h"
 #include "mf_launch.h"
+
+// Host copy pool for the pageable-buffer path: a few persistent threads that split one
+// memcpy (or a strided row copy) between them.  One pool per context; run() blocks until
+// every piece is done.
+struct CopyPool {
+  std::vector<std::thread> threads;
+  std::mutex mu;
+  std::condition_variable cv, done_cv;
+  std::function<void(int)> job;
+  int parts = 0, next = 0, remaining = 0;
+  uint64_t gen = 0;
+  bool stop = false;
+  explicit CopyPool(int n) {
+    for (int i = 0; i < n; ++i) threads.emplace_back([this] { loop(); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> l(mu);
+      stop = true;
+    }
+    cv.notify_all();
+    for (auto& t : threads) t.join();
+  }
+  int size() const { return (int)threads.size() + 1; }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> l(mu);
+      cv.wait(l, [&] { return stop || (gen != seen && next < parts); });
+      if (stop) return;
+      seen = gen;
+      while (next < parts) {
+        const int i = next++;
+        l.unlock();
+        job(i);
+        l.lock();
+        if (--remaining == 0) done_cv.notify_all();
+      }
+    }
+  }
+  // job(i) for i in [0, n), on the pool and the calling thread
+  void run(int n, std::function<void(int)> f) {
+    if (n <= 1 || threads.empty()) {
+      for (int i = 0; i < n; ++i) f(i);
+      return;
+    }
+    std::unique_lock<std::mutex> l(mu);
+    job = std::move(f);
+    parts = n;
+    next = 0;
+    remaining = n;
+    ++gen;
+    cv.notify_all();
+    while (next < parts) {  // the caller takes pieces too
+      const int i = next++;
+      l.unlock();
+      job(i);
+      l.lock();
+      --remaining;
+    }
+    done_cv.wait(l, [&] { return remaining == 0; });
+  }
+  // rows x bytes strided copy, split by rows (or by bytes for one row)
+  void copy2d(char* dst, size_t dld, const char* src, size_t sld, size_t bytes, size_t rows) {
+    constexpr size_t kPiece = size_t(1) << 20;
+    const size_t total = bytes * rows;
+    const int n = (int)std::max<size_t>(1, std::min<size_t>((size_t)size(), total / kPiece));
+    if (rows == 1) {
+      run(n, [&](int i) {
+        const size_t a = bytes * i / n, b = bytes * (i + 1) / n;
+        std::memcpy(dst + a, src + a, b - a);
+      });
+    } else {
+      const int m = (int)std::min<size_t>(rows, (size_t)n);
+      run(m, [&](int i) {
+        for (size_t r = rows * i / m; r < rows * (i + 1) / m; ++r) std::memcpy(dst + r * dld, src + r * sld, bytes);
+      });
+    }
+  }
+};
 
 struct mf_context {
   int device = 0;
@@ -33,6 +115,10 @@ struct mf_context {
   // streams, so concurrent large-k calls on two streams never overlap on ws)
   cudaEvent_t ws_ev = nullptr;
   bool ws_ev_recorded = false;
+  // pageable host buffers: pinned staging slots and the copy pool (created on first use)
+  void* hstage = nullptr;
+  size_t hstage_bytes = 0;
+  CopyPool* pool = nullptr;
   // multi-device context (mf_context_create_multi): one sub-context per device; the host
   // entries shard their work over them.  Empty for a single-device context.
   std::vector<mf_context*> subs;
@@ -60,6 +146,16 @@ mf_status grow(void** p, size_t* cap, size_t need) {
   if (e != cudaSuccess) { cudaGetLastError(); return from_cuda(e); }
   *cap = need;
   return MF_OK;
+}
+
+// Host memory the DMA engines can read directly: pinned (cudaHostAlloc) or registered.
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
 }
 
 // Order a use of ctx->ws on stream s after the previous use (on whatever stream).
@@ -234,6 +330,8 @@ void mf_context_destroy(mf_context* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->ws_ev) cudaEventDestroy(ctx->ws_ev);
+  if (ctx->hstage) cudaFreeHost(ctx->hstage);
+  delete ctx->pool;
   if (ctx->io) cudaFree(ctx->io);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->s_h2d) cudaStreamSynchronize(ctx->s_h2d), cudaStreamDestroy(ctx->s_h2d);
@@ -393,7 +491,7 @@ mf_status mf_median_filter_rows(mf_context* ctx, mf_dtype dtype, const void* x, 
   // ramp up geometrically at the start and down at the end, so the H2D of the first chunk
   // and the D2H of the last (the parts nothing overlaps) are small.
   const bool by_rows = rows > 1;
-  const size_t total = by_rows ? rows : keep;                                               // units to cut
+  const size_t total = by_rows ? rows : keep;  // units to cut
   const size_t cmax = by_rows ? std::max<size_t>(1, kChunkElems / n) : std::min(keep, std::max<size_t>(kChunkElems, 16 * k));
   const size_t cmin = std::max<size_t>(by_rows ? 1 : std::min(cmax, 16 * k), cmax / MF_PIPE_RAMP);
   std::vector<size_t> sizes = chunk_schedule(total, cmin, cmax);
@@ -403,12 +501,47 @@ mf_status mf_median_filter_rows(mf_context* ctx, mf_dtype dtype, const void* x, 
   const int slots = (int)std::min<size_t>(kNumSlots, nchunks);
   st = grow(&ctx->io, &ctx->io_bytes, slots * (in_slot + out_slot));
   if (st != MF_OK) return st;
+  // Pageable caller buffers (e.g. a std::vector behind gpu.hpp): the DMA engines cannot read
+  // them directly, and the driver's own staging serialises the copy with the host thread.
+  // They go through pinned staging slots instead, filled and drained by the context's copy
+  // pool: the host copies chunk c+1 in and chunk c-1 out while the device runs chunk c.
+  const bool stage_in = !host_pinned(x), stage_out = !host_pinned(y);
+  char* hin = nullptr;
+  char* hout = nullptr;
+  if (stage_in || stage_out) {
+    const size_t need = slots * (in_slot + out_slot);
+    if (need > ctx->hstage_bytes) {
+      if (ctx->hstage) cudaFreeHost(ctx->hstage);
+      ctx->hstage = nullptr;
+      ctx->hstage_bytes = 0;
+      if (cudaHostAlloc(&ctx->hstage, need, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        return MF_OUT_OF_MEMORY;
+      }
+      ctx->hstage_bytes = need;
+    }
+    if (!ctx->pool) {
+      const unsigned hc = std::max(2u, std::thread::hardware_concurrency());
+      ctx->pool = new CopyPool((int)std::min(15u, hc - 1));
+    }
+    hin = static_cast<char*>(ctx->hstage);
+    hout = hin + slots * in_slot;
+  }
   char* base = static_cast<char*>(ctx->io);
   const char* hx = static_cast<const char*>(x);
   char* hy = static_cast<char*>(y);
   uint64_t launches = 0;
-  size_t start = 0;
   cudaError_t e = cudaSuccess;
+  // chunk geometry: [begin unit, units) of chunk c
+  std::vector<size_t> starts(nchunks + 1, 0);
+  for (size_t c = 0; c < nchunks; ++c) starts[c + 1] = starts[c] + sizes[c];
+  auto copy_out = [&](size_t c) {  // staged outputs of chunk c -> caller buffer
+    const int sl = (int)(c % slots);
+    const char* src = hout + sl * out_slot;
+    if (by_rows) ctx->pool->copy2d(hy + starts[c] * ld_y * w, ld_y * w, src, keep * w, keep * w, sizes[c]);
+    else ctx->pool->copy2d(hy + starts[c] * w, 0, src, 0, sizes[c] * w, 1);
+  };
+  size_t drained = 0;  // chunks whose outputs reached the caller's buffer (staged outputs)
   for (size_t c = 0; c < nchunks && e == cudaSuccess; ++c) {
     const int sl = (int)(c % slots);
     char* d_x = base + sl * (in_slot + out_slot);
@@ -419,17 +552,24 @@ mf_status mf_median_filter_rows(mf_context* ctx, mf_dtype dtype, const void* x, 
     }
     size_t r0 = 0, nr = 1, o0 = 0, no = keep, ni = n;
     if (by_rows) {
-      r0 = start;
+      r0 = starts[c];
       nr = sizes[c];
+    } else {
+      o0 = starts[c];
+      no = sizes[c];
+      ni = no + k - 1;
+    }
+    if (stage_in) {  // pageable -> pinned slot (its previous H2D finished: see below)
+      char* hs = hin + sl * in_slot;
+      if (by_rows) ctx->pool->copy2d(hs, n * w, hx + r0 * ld_x * w, ld_x * w, n * w, nr);
+      else ctx->pool->copy2d(hs, 0, hx + o0 * w, 0, ni * w, 1);
+      e = cudaMemcpyAsync(d_x, hs, (by_rows ? nr * n : ni) * w, cudaMemcpyHostToDevice, ctx->s_h2d);
+    } else if (by_rows) {
       e = cudaMemcpy2DAsync(d_x, n * w, hx + r0 * ld_x * w, ld_x * w, n * w, nr, cudaMemcpyHostToDevice,
                             ctx->s_h2d);
     } else {
-      o0 = start;
-      no = sizes[c];
-      ni = no + k - 1;
       e = cudaMemcpyAsync(d_x, hx + o0 * w, ni * w, cudaMemcpyHostToDevice, ctx->s_h2d);
     }
-    start += sizes[c];
     if (e != cudaSuccess) break;
     if ((e = cudaEventRecord(ctx->ev_in[sl], ctx->s_h2d)) != cudaSuccess) break;
     if ((e = cudaStreamWaitEvent(ctx->stream, ctx->ev_in[sl], 0)) != cudaSuccess) break;
@@ -438,17 +578,31 @@ mf_status mf_median_filter_rows(mf_context* ctx, mf_dtype dtype, const void* x, 
     if (st != MF_OK) break;
     if ((e = cudaEventRecord(ctx->ev_done[sl], ctx->stream)) != cudaSuccess) break;
     if ((e = cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_done[sl], 0)) != cudaSuccess) break;
-    if (by_rows)
+    if (stage_out) {
+      e = cudaMemcpyAsync(hout + sl * out_slot, d_y, (by_rows ? nr * keep : no) * w, cudaMemcpyDeviceToHost,
+                          ctx->s_d2h);
+    } else if (by_rows) {
       e = cudaMemcpy2DAsync(hy + r0 * ld_y * w, ld_y * w, d_y, keep * w, keep * w, nr, cudaMemcpyDeviceToHost,
                             ctx->s_d2h);
-    else
+    } else {
       e = cudaMemcpyAsync(hy + o0 * w, d_y, no * w, cudaMemcpyDeviceToHost, ctx->s_d2h);
+    }
     if (e != cudaSuccess) break;
-    e = cudaEventRecord(ctx->ev_out[sl], ctx->s_d2h);
+    if ((e = cudaEventRecord(ctx->ev_out[sl], ctx->s_d2h)) != cudaSuccess) break;
+    // Host side of the staged path, while the device runs chunk c: drain chunk c-1's outputs.
+    // Waiting for chunk c-1's D2H also retires every H2D up to c-1, so the pinned input slot
+    // of chunk c+1 (that of chunk c+1-slots) is free when the next iteration fills it.
+    if ((stage_in || stage_out) && c >= 1) {
+      if ((e = cudaEventSynchronize(ctx->ev_out[(c - 1) % slots])) != cudaSuccess) break;
+      if (stage_out) copy_out(c - 1);
+      drained = c;
+    }
   }
   ctx->launches = launches;
   const cudaError_t e2 = cudaStreamSynchronize(ctx->s_d2h);
   const cudaError_t e3 = cudaStreamSynchronize(ctx->stream);
+  if (st == MF_OK && e == cudaSuccess && e2 == cudaSuccess && stage_out)
+    for (size_t c = drained; c < nchunks; ++c) copy_out(c);
   if (st != MF_OK) return st;
   if (e != cudaSuccess) return from_cuda(e);
   if (e2 != cudaSuccess) return from_cuda(e2);
