@@ -154,6 +154,7 @@ __device__ __noinline__ void compact_block(E* sb, int NS, uint32_t k, uint32_t l
     const bool real = e.idx() < k;
     const uint32_t bal = __ballot_sync(0xFFFFFFFFu, real);
     __syncwarp();
+    MF_ASSERT(!real || base + __popc(bal & ((1u << lane) - 1u)) < k);
     if (real) sb[pad<PS>((int)(base + __popc(bal & ((1u << lane) - 1u))))] = e;
     base += __popc(bal);
     __syncwarp();
@@ -249,6 +250,7 @@ constexpr uint32_t cpad5(uint32_t q) { return q + (q >> 5); }
 // Plain (reorderable) shared load by shared-window address.  It is ordered after a barrier
 // only through its address: callers add order_token(), read after the barrier.
 __device__ __forceinline__ uint32_t lds32(uint32_t saddr) {
+  check_saddr(saddr, 4);
   uint32_t v;
   asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr));
   return v;
@@ -383,9 +385,13 @@ __device__ __forceinline__ void team_sort_keys(KElem32* sb, const typename Trait
     const uint32_t e = sub * NS + lane + 32 * r;
     const bool real = e < k;
     maxkey |= real && key[r] == 0xFFFFFFFFu;
+    MF_ASSERT(!real || pos[r] < k);
+    check_sptr(&cnt[real ? pos[r] : BS - 1]);
     const uint32_t t = atomicAdd(&cnt[real ? pos[r] : BS - 1], 1u);
     uint32_t ri = e;
     if constexpr (SRr > 0) ri = (e & (SRr - 1)) * CHr + e / SRr;
+    MF_ASSERT(!real || pos[r] + t < k);
+    check_sptr(&sb[pad<PS>((int)(real ? pos[r] + t : BS))]);
     sb[pad<PS>((int)(real ? pos[r] + t : BS))] = KElem32::make(key[r], ri);
   }
   // the scratch is reused by the next sort

@@ -14,11 +14,59 @@
 // sentinel takes (core.hpp:34-47).  No kept window ever contains padding
 // (filter.hpp:76-79), so padding never reaches an output.
 #pragma once
+#include <cassert>
 #include <cstdint>
 #include <type_traits>
 #include <cuda_runtime.h>
 
+// MF_CHECK=1 builds (paper_1406_1717_b200.build.build(extra_flags=["-DMF_CHECK=1"], ...)):
+// every data-dependent shared-memory index and every output store is bounds-checked with a
+// device assert (file/line printed, kernel trapped).  compute-sanitizer is not available on
+// the GPU pool, so the GPU suite run against this build is the memory-safety evidence
+// (profiles/r02_checked_build.txt).  Release builds compile the checks away.
+#ifndef MF_CHECK
+#define MF_CHECK 0
+#endif
+#if MF_CHECK
+#define MF_ASSERT(...) assert((__VA_ARGS__))
+#else
+#define MF_ASSERT(...) ((void)0)
+#endif
+
 namespace mf {
+
+// size in bytes of the launch's dynamic shared memory (checked builds)
+__device__ __forceinline__ uint32_t dyn_smem_bytes() {
+  uint32_t v;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(v));
+  return v;
+}
+// `saddr` (shared-window byte address) .. saddr + bytes lies inside the dynamic smem that
+// starts at shared-window address `base`
+__device__ __forceinline__ void check_smem(uint32_t base, uint32_t saddr, uint32_t bytes) {
+  MF_ASSERT(saddr >= base && saddr + bytes <= base + dyn_smem_bytes());
+  (void)base; (void)saddr; (void)bytes;
+}
+#if MF_CHECK
+extern __shared__ __align__(16) unsigned char mf_dyn_smem[];  // aliases every kernel's dynamic smem
+#endif
+// shared-window address `saddr` .. + bytes inside the launch's dynamic shared memory
+__device__ __forceinline__ void check_saddr(uint32_t saddr, uint32_t bytes) {
+#if MF_CHECK
+  check_smem((uint32_t)__cvta_generic_to_shared(mf_dyn_smem), saddr, bytes);
+#else
+  (void)saddr; (void)bytes;
+#endif
+}
+// p .. p + count elements inside the launch's dynamic shared memory
+template <typename P>
+__device__ __forceinline__ void check_sptr(const P* p, uint32_t count = 1) {
+#if MF_CHECK
+  check_saddr((uint32_t)__cvta_generic_to_shared(p), (uint32_t)(sizeof(P) * count));
+#else
+  (void)p; (void)count;
+#endif
+}
 
 enum DType : int { DT_I32 = 0, DT_I64 = 1, DT_F32 = 2, DT_F64 = 3 };
 

@@ -486,8 +486,11 @@ __global__ void __launch_bounds__(LNT, 4) ml_unit_merge(LargeGeom L, const Elem<
       sk[pad<LPS>(dd + r)] = v[r].key();
       so[pad<LPS>(dd + r)] = idx | (srcB[r] ? 0x80000000u : 0u);
       uint2* slot = ro + (uint64_t)(idx & (L.CL - 1)) * C + (idx >> L.CLshift);  // transposed [t][c]
+      MF_ASSERT(idx < k && q < L.nq && (idx >> L.CLshift) < C);
       if (srcB[r]) slot->y = q; else slot->x = q;
       const uint32_t sw = (dd + r) >> 10;                   // superword within the tile
+      MF_ASSERT(sw < 4);
+      check_sptr(&hist[(sw * 2 + (srcB[r] ? 1 : 0)) * C + (idx >> L.CLshift)]);
       atomicAdd(&hist[(sw * 2 + (srcB[r] ? 1 : 0)) * C + (idx >> L.CLshift)], 1u);
     }
   }
@@ -613,6 +616,7 @@ __global__ void __launch_bounds__(LNT) ml_walk(LargeGeom L, const typename Trait
     uint32_t r = h - acc;
     uint32_t cw = S * 32, cb = 0;
     for (;; ++cw) {
+      MF_ASSERT(cw < nwq);
       cb = live_word(og, cw, i0, L.nq);
       const uint32_t pc = __popc(cb);
       if (r < pc) break;
@@ -632,6 +636,7 @@ __global__ void __launch_bounds__(LNT) ml_walk(LargeGeom L, const typename Trait
         if (t > 0) {
           const uint2 ab = __ldg(rb + (uint64_t)(t - 1) * L.C);
           const uint32_t a = ab.x, b = ab.y;
+          MF_ASSERT(a < L.nq && b < L.nq);
           const uint32_t base = cw0 * 32;
           const uint32_t oa = a - base, ob = b - base, off = p - base;   // window offsets
           win &= ~(oa < 64 ? 1ull << oa : 0ull);
@@ -654,6 +659,7 @@ __global__ void __launch_bounds__(LNT) ml_walk(LargeGeom L, const typename Trait
           }
           p = sel(up, cw0 * 32 + __ffsll((long long)m) - 1, sel(down, cw0 * 32 + 63 - __clzll((long long)m), p));
         }
+        MF_ASSERT(p < L.nq);
         stage[lane * 9 + tt] = __ldg(mkg + p);
       }
     }
@@ -664,7 +670,10 @@ __global__ void __launch_bounds__(LNT) ml_walk(LargeGeom L, const typename Trait
       const uint32_t src = 4 * j + (lane >> 3), st = lane & 7;
       const uint32_t jn = __shfl_sync(0xFFFFFFFFu, my_n, src);
       TV* yj = reinterpret_cast<TV*>(__shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(y), src));
-      if (t0 + st < jn) yj[t0 + st] = Tr::dec(stage[src * 9 + st]);
+      if (t0 + st < jn) {
+        MF_ASSERT(yj + t0 + st < reinterpret_cast<TV*>(g.y) + (uint64_t)(g.rows - 1) * g.ld_y + g.keep);
+        yj[t0 + st] = Tr::dec(stage[src * 9 + st]);
+      }
     }
     __syncwarp();
     if (__all_sync(0xFFFFFFFFu, t0 + 8 >= my_n)) break;

@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
         }
       };
       auto at = [&](uint32_t off) -> uint2 {
+        check_saddr(ringS + off, 8);
         uint2 v;
         asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(ringS + off));
         return v;
@@ -247,6 +248,9 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
           // past the pair both sides are the sentinel: ridx clamps to BS-1 >= k, whose rab
           // entry and row bits beyond 2k nobody reads -- no branch
           const uint32_t ri = min(takeA ? ea[j].x : eb[j].x, (uint32_t)C::BS - 1);
+          MF_ASSERT(w0 < (uint32_t)C::NWP && src_slot<PL, 32 * WP>(q) < 2u * C::BS);
+          check_sptr(&rows[row_addr<CH, C::NWP>(ri & (CH - 1), w0)]);
+          check_sptr(&rab16[2 * ri + 1]);
           atomicOr(&rows[row_addr<CH, C::NWP>(ri & (CH - 1), w0)], bit[j]);
           src[src_slot<PL, 32 * WP>(q)] = (uint16_t)((takeA ? relA[j] : relB[j]) + 4);
           rab16[2 * ri + (takeA ? 0 : 1)] = (uint16_t)q;
@@ -383,6 +387,8 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
         auto key_at = [&](uint32_t p) -> U {
           if constexpr (C::KS) {
             uint32_t v;
+            MF_ASSERT(p < nq && src_slot<PL, TL>(p) < 2u * C::BS);
+            check_saddr(ringK + src[src_slot<PL, TL>(p)], 4);
             asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(ringK + src[src_slot<PL, TL>(p)]));
             return (U)v;
           } else if constexpr (C::MK) {
@@ -430,6 +436,7 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
             if (i0 + t < imax) {
               const uint32_t ab = rab[(t - 1) * CH + tl];
               const uint32_t a = ab & 0xFFFF, b = ab >> 16;
+              MF_ASSERT(a < nq && b < nq && tl < (uint32_t)CH);
               const uint32_t ba = 1u << (a & 31), bb = 1u << (b & 31);
               // Delete(A, i-1) and Undelete(B, i-1), written through to the row in shared
               // memory (fire-and-forget atomics, no divergence) and to the cached cursor word
@@ -446,7 +453,12 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
               uint32_t m = sel(up, mu, md);
               if ((up || down) && m == 0) {  // the next live position is in another word (rare)
                 const int dir = up ? 1 : -1;
-                do { cw += dir; cb = rows[row_addr<CH, C::NWP>(tl, cw)]; m = cb; } while (m == 0);
+                do {
+                  cw += dir;
+                  MF_ASSERT(cw < nw);
+                  cb = rows[row_addr<CH, C::NWP>(tl, cw)];
+                  m = cb;
+                } while (m == 0);
               }
               p = sel(up, cw * 32 + __ffs(m) - 1, sel(down, cw * 32 + 31 - __clz(m), p));
               out[t] = key_at(p);
@@ -456,9 +468,13 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
         team_sync();  // rows are dead: reuse them as the output staging area
 #pragma unroll
         for (int t = 0; t < SR; ++t)
-          if (i0 + t < imax) ost[i0 + t + ((i0 + t) >> 5)] = out[t];
+          if (i0 + t < imax) {
+            check_sptr(&ost[i0 + t + ((i0 + t) >> 5)]);
+            ost[i0 + t + ((i0 + t) >> 5)] = out[t];
+          }
         team_sync();
         TV* yo = y + u * k;
+        MF_ASSERT(u * k + imax <= g.keep);
         for (uint32_t i = tl; i < imax; i += TL) yo[i] = Tr::dec(ost[i + (i >> 5)]);
       }
     }

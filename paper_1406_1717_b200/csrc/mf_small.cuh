@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_
       sort_regs<K>(v);
 #pragma unroll
       for (int p = 0; p < K; ++p) {
+        MF_ASSERT(v[p].idx() < (uint32_t)K && c < (uint32_t)SC);
         skey[p * SC + c] = v[p].key();
         srank[v[p].idx() * SC + c] = (uint8_t)p;
       }
@@ -228,6 +229,7 @@ __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_
       for (int i = 1; i < K; ++i) {
         const uint32_t ra = rA[(i - 1) * SC];
         const uint32_t rb = rB[(i - 1) * SC];
+        MF_ASSERT(ra < KK && rb < KK);
         // Delete(A, i-1): block.hpp:71-87
         maskA &= ~((M)1 << ra);
         const bool belowA = ra < mA;
@@ -271,6 +273,8 @@ __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_
       constexpr int EPC = 16 / (int)sizeof(U);
       const uint64_t left = g.keep > obase ? g.keep - obase : 0;
       const uint32_t n_out = (uint32_t)(left < (uint64_t)TU * K ? left : (uint64_t)TU * K);
+      MF_ASSERT(obase + n_out <= g.keep);
+      check_sptr(ost, n_out);
       const uint32_t head = min((uint32_t)((EPC - omis) % EPC), n_out);
       const uint32_t nvec = (n_out - head) / EPC;
       TV* yo = y + obase;
