@@ -51,6 +51,8 @@ cudaError_t configure(const LargeGeom& L) {
   for (auto f : {ml_tile_sort<DT, true>, ml_tile_sort<DT, false>})
     if ((e = kernel_setup((const void*)f, TileSort<U>::smem, 0, nullptr)) != cudaSuccess) return e;
   if ((e = kernel_setup((const void*)ml_tile_radix<DT>, TileRadix<U>::smem, 0, nullptr)) != cudaSuccess) return e;
+  if constexpr (sizeof(U) == 8)
+    if ((e = kernel_setup((const void*)ml_tile_sort_soa<DT>, TileSoa::smem, 0, nullptr)) != cudaSuccess) return e;
   for (auto f : {ml_merge_pass<DT, true>, ml_merge_pass<DT, false>})
     if ((e = kernel_setup((const void*)f, merge_tile_smem<U>(), 0, nullptr)) != cudaSuccess) return e;
   if ((e = kernel_setup((const void*)ml_walk<DT>, sizeof(U) * 32 * 9 * (LNT / 32), 0, nullptr)) != cudaSuccess)
@@ -99,7 +101,11 @@ cudaError_t sort_blocks(const LargeGeom& L, unsigned char* ws, const Layout<DT>&
   ml_tile_radix<DT><<<dim3((unsigned)(L.nb * L.tiles), L.g.rows), TileRadix<U>::NT, TileRadix<U>::smem, s>>>(
       L, bufs[0]);
 #else
-  ml_tile_sort<DT, KO><<<dim3((unsigned)(L.nb * L.tiles), L.g.rows), LNT, TileSort<U>::smem, s>>>(L, bufs[0]);
+  if constexpr (MF_TS_SOA && KO && sizeof(U) == 8)
+    ml_tile_sort_soa<DT><<<dim3((unsigned)(L.nb * L.tiles), L.g.rows), LNT, TileSoa::smem, s>>>(
+        L, reinterpret_cast<Elem<uint64_t>*>(bufs[0]));
+  else
+    ml_tile_sort<DT, KO><<<dim3((unsigned)(L.nb * L.tiles), L.g.rows), LNT, TileSort<U>::smem, s>>>(L, bufs[0]);
 #endif
   ++*launches;
   int cur = 0;

@@ -174,6 +174,140 @@ __device__ __forceinline__ void store_elem(Elem<uint64_t>* o, uint64_t key, uint
   *reinterpret_cast<uint4*>(o) = make_uint4((uint32_t)key, (uint32_t)(key >> 32), idx, 0u);
 }
 
+// ---- phase 1a, 64-bit keys in key order: struct-of-arrays tile sort ------------------------
+// The filter's tile sort for 64-bit keys keeps keys and indices in two padded shared
+// arrays instead of 16-byte {key, index} elements: a merge step compares keys only (one
+// 8-byte load refills the consumed side), and the index of the taken element is loaded off
+// the dependency chain.  8-byte keys at the pad<4> stride store conflict-free, and the tile
+// takes 12 bytes per element of shared memory instead of 16.  Ties between equal keys may
+// land in any order (key order, KElem64); the slot fillers of the last tile are compacted
+// as in ml_tile_sort.
+#ifndef MF_TS_SOA
+#define MF_TS_SOA 1
+#endif
+#ifndef MF_TS_SOA_MINB
+#define MF_TS_SOA_MINB 3
+#endif
+struct TileSoa {
+  static constexpr int R = 16, PS = 4, TS = 8 * 32 * R;
+  static constexpr int NSLOT = TS + (TS >> PS) + 1;
+  static constexpr size_t smem = (sizeof(uint64_t) + sizeof(uint32_t)) * NSLOT + sizeof(uint32_t) * (LNT / 32);
+};
+
+// Merge-path levels over the SoA arrays (runs run0, 2*run0, ... < run_end); thread `tid`
+// produces outputs [j*R, j*R + R) of its merged run pair.  Key compares are strict in both
+// the search and the steps, so the lanes' ranges tile each merged run exactly.
+template <int R, int PS, typename Sync>
+__device__ __forceinline__ void merge_levels_soa(uint64_t* sk, uint32_t* si, int b0, int tid, int run0, int run_end,
+                                                 uint64_t (&vk)[R], uint32_t (&vi)[R], Sync sync) {
+#pragma unroll 1
+  for (int run = run0; run < run_end; run *= 2) {
+    const int gl = (2 * run) / R;                // threads per merged run
+    const int j = tid & (gl - 1);
+    const int xb = b0 + (tid / gl) * (2 * run);  // X = [xb, xb+run), Y = [xb+run, xb+2run)
+    const int yb0 = xb + run;
+    const int d = j * R;
+    int lo = d > run ? d - run : 0, hi = d < run ? d : run;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (sk[pad<PS>(xb + mid)] < sk[pad<PS>(yb0 + d - 1 - mid)]) lo = mid + 1; else hi = mid;
+    }
+    int ia = lo, ib = d - lo;
+    uint64_t xa = sk[pad<PS>(xb + min(ia, run - 1))], yv = sk[pad<PS>(yb0 + min(ib, run - 1))];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const bool takeA = (ib >= run) || (ia < run && xa < yv);
+      vk[r] = takeA ? xa : yv;
+      vi[r] = si[pad<PS>(takeA ? xb + ia : yb0 + ib)];   // off the chain
+      ia += takeA;
+      ib += !takeA;
+      const uint64_t nv = sk[pad<PS>(takeA ? xb + min(ia, run - 1) : yb0 + min(ib, run - 1))];
+      xa = takeA ? nv : xa;
+      yv = takeA ? yv : nv;
+    }
+    sync();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      sk[pad<PS>(xb + d + r)] = vk[r];
+      si[pad<PS>(xb + d + r)] = vi[r];
+    }
+    sync();
+  }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(LNT, MF_TS_SOA_MINB) ml_tile_sort_soa(LargeGeom L, Elem<uint64_t>* out) {
+  using Tr = Traits<DT>;
+  using TV = typename Tr::T;
+  static_assert(sizeof(typename Tr::U) == 8, "64-bit keys");
+  constexpr int R = TileSoa::R, PS = TileSoa::PS, TS = TileSoa::TS, NSLOT = TileSoa::NSLOT;
+  static_assert(TS == TileSort<uint64_t>::TS, "same tiles as the merge passes expect");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* si = reinterpret_cast<uint32_t*>(sk + NSLOT);
+  uint32_t* wsum = si + NSLOT;
+  const Geom& g = L.g;
+  const uint64_t row = blockIdx.y;
+  const uint64_t b = blockIdx.x / L.tiles;
+  const uint32_t t = blockIdx.x % L.tiles;
+  const TV* x = reinterpret_cast<const TV*>(g.x) + row * g.ld_x;
+  const uint32_t k = g.k;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  {
+    KElem64 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t e = t * TS + warp * 32 * R + lane + 32 * r;  // coalesced across the warp
+      const uint64_t gp = b * k + e;
+      const uint64_t key = (e < k && gp < g.n) ? Tr::enc(__ldg(x + gp)) : UMax<uint64_t>::v;
+      v[r] = KElem64::make(key, e);
+    }
+    sort_regs<R>(v);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int p = pad<PS>((int)(warp * 32 * R + lane * R + r));
+      sk[p] = v[r].k;
+      si[p] = v[r].i;
+    }
+  }
+  __syncwarp();
+  uint64_t vk[R];
+  uint32_t vi[R];
+  merge_levels_soa<R, PS>(sk, si, warp * 32 * R, lane, R, 32 * R, vk, vi, SyncWarp{});
+  __syncthreads();
+  merge_levels_soa<R, PS>(sk, si, 0, threadIdx.x, 32 * R, TS, vk, vi, SyncCta{});
+  const uint32_t len = min((uint32_t)TS, k - t * TS);
+  Elem<uint64_t>* o = out + (row * L.nb + b) * k + (uint64_t)t * TS;
+  if (len == (uint32_t)TS) {
+    for (uint32_t i = threadIdx.x; i < len; i += LNT) store_elem(o + i, sk[pad<PS>(i)], si[pad<PS>(i)]);
+    return;
+  }
+  // last tile of a block: keep the real elements (index < k) in sorted order (see ml_tile_sort)
+  constexpr int RUN = TS / LNT;
+  const uint32_t i0 = threadIdx.x * RUN;
+  uint32_t c = 0;
+#pragma unroll 4
+  for (int j = 0; j < RUN; ++j) c += si[pad<PS>(i0 + j)] < k;
+  uint32_t inc = c;
+#pragma unroll
+  for (int dd = 1; dd < 32; dd <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, dd);
+    if (lane >= (uint32_t)dd) inc += y;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  uint32_t q = inc - c;
+  for (uint32_t w = 0; w < warp; ++w) q += wsum[w];
+#pragma unroll 4
+  for (int j = 0; j < RUN; ++j) {
+    const uint32_t e = si[pad<PS>(i0 + j)];
+    if (e < k) {
+      MF_ASSERT(q < len);
+      store_elem(o + q++, sk[pad<PS>(i0 + j)], e);
+    }
+  }
+}
+
 template <int DT>
 __global__ void __launch_bounds__(TileRadix<typename Traits<DT>::U>::NT, TileRadix<typename Traits<DT>::U>::MINB)
     ml_tile_radix(LargeGeom L, Elem<typename Traits<DT>::U>* out) {
