@@ -53,11 +53,14 @@ cudaError_t configure(const LargeGeom& L) {
   if ((e = kernel_setup((const void*)ml_tile_radix<DT>, TileRadix<U>::smem, 0, nullptr)) != cudaSuccess) return e;
   if constexpr (sizeof(U) == 8)
     if ((e = kernel_setup((const void*)ml_tile_sort_soa<DT>, TileSoa::smem, 0, nullptr)) != cudaSuccess) return e;
-  for (auto f : {ml_merge_pass<DT, true>, ml_merge_pass<DT, false>})
-    if ((e = kernel_setup((const void*)f, merge_tile_smem<U>(), 0, nullptr)) != cudaSuccess) return e;
+  if ((e = kernel_setup((const void*)ml_merge_pass<DT, true>, merge_tile_bytes<U, kSoa<U, true>>(), 0, nullptr)) !=
+      cudaSuccess)
+    return e;
+  if ((e = kernel_setup((const void*)ml_merge_pass<DT, false>, merge_tile_smem<U>(), 0, nullptr)) != cudaSuccess)
+    return e;
   if ((e = kernel_setup((const void*)ml_walk<DT>, sizeof(U) * 32 * 9 * (LNT / 32), 0, nullptr)) != cudaSuccess)
     return e;
-  const size_t um = merge_tile_smem<U>() + sizeof(uint32_t) * 8 * L.C;
+  const size_t um = merge_tile_bytes<U, kSoa<U, true>>() + sizeof(uint32_t) * 8 * L.C;
   return kernel_setup((const void*)ml_unit_merge<DT>, um, 0, nullptr);
 }
 
@@ -114,7 +117,7 @@ cudaError_t sort_blocks(const LargeGeom& L, unsigned char* ws, const Layout<DT>&
   for (uint64_t run = L.TS; run < L.g.k; run *= 2) {
     ml_partition_pass<DT, KO><<<(unsigned)((ptiles + 127) / 128), 128, 0, s>>>(L, bufs[cur], splits, (uint32_t)run,
                                                                          ptiles);
-    ml_merge_pass<DT, KO><<<dim3((unsigned)(L.nb * L.mtiles), L.g.rows), LNT, merge_tile_smem<U>(), s>>>(
+    ml_merge_pass<DT, KO><<<dim3((unsigned)(L.nb * L.mtiles), L.g.rows), LNT, merge_tile_bytes<U, kSoa<U, KO>>(), s>>>(
         L, bufs[cur], bufs[cur ^ 1], (uint32_t)run, splits);
     *launches += 2;
     cur ^= 1;
@@ -138,7 +141,7 @@ cudaError_t run_large_dt(const Geom& g, void* wsv, size_t ws_bytes, cudaStream_t
   uint2* rab = reinterpret_cast<uint2*>(ws + lay.off_rab);
   uint32_t* live = reinterpret_cast<uint32_t*>(ws + lay.off_live);
   const uint64_t nu = (uint64_t)g.rows * g.units;
-  const size_t um = merge_tile_smem<U>() + sizeof(uint32_t) * 8 * L.C;
+  const size_t um = merge_tile_bytes<U, kSoa<U, true>>() + sizeof(uint32_t) * 8 * L.C;
   uint2* splits = reinterpret_cast<uint2*>(ws + lay.off_split);
   const uint64_t utiles = (uint64_t)g.rows * g.units * L.tiles2;
   ml_partition_units<DT><<<(unsigned)((utiles + 127) / 128), 128, 0, s>>>(L, sorted, splits, utiles);

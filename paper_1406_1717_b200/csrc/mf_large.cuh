@@ -31,6 +31,18 @@ constexpr int LQ = LNT * LR2;    // merge tile (elements), a multiple of 1024
 constexpr int LPS = 4;           // pad shift of merge tiles (R = 16)
 template <typename U>
 constexpr size_t merge_tile_smem() { return sizeof(Elem<U>) * (LQ + (LQ >> LPS) + 1); }
+// 64-bit keys in key order (the filter's passes, not the phase API) keep their tiles as
+// struct-of-arrays in shared memory: keys and indices in two padded arrays, 12 bytes per
+// element instead of 16, key-only merge compares (ml_tile_sort_soa, merge_tile_soa).
+#ifndef MF_TS_SOA
+#define MF_TS_SOA 1
+#endif
+template <typename U, bool KO>
+constexpr bool kSoa = MF_TS_SOA && KO && sizeof(U) == 8;
+template <typename U, bool SOA>
+constexpr size_t merge_tile_bytes() {
+  return (SOA ? sizeof(U) + sizeof(uint32_t) : sizeof(Elem<U>)) * (LQ + (LQ >> LPS) + 1);
+}
 
 // tile sort geometry by key width: 8 warps x 32R elements
 template <typename U> struct TileSortCfg;
@@ -182,9 +194,6 @@ __device__ __forceinline__ void store_elem(Elem<uint64_t>* o, uint64_t key, uint
 // takes 12 bytes per element of shared memory instead of 16.  Ties between equal keys may
 // land in any order (key order, KElem64); the slot fillers of the last tile are compacted
 // as in ml_tile_sort.
-#ifndef MF_TS_SOA
-#define MF_TS_SOA 1
-#endif
 #ifndef MF_TS_SOA_MINB
 #define MF_TS_SOA_MINB 3
 #endif
@@ -486,6 +495,66 @@ __device__ __forceinline__ int merge_tile(E* s, const E* X, const E* Y, uint32_t
   return cnt;
 }
 
+// merge_tile over struct-of-arrays shared tiles (64-bit keys): keys in sk, indices in si,
+// key compares only (LE: x goes first on ties, else y does); the taken element's index is
+// loaded off the dependency chain.
+template <bool LE, typename E>
+__device__ __forceinline__ int merge_tile_soa(uint64_t* sk, uint32_t* si, const E* X, const E* Y, uint32_t d0,
+                                              uint32_t d1, uint2 sp, uint64_t (&vk)[LR2], uint32_t (&vi)[LR2],
+                                              bool (&srcB)[LR2], uint32_t& nx_out) {
+  const uint32_t a0 = sp.x, a1 = sp.y;
+  const uint32_t b0 = d0 - a0, b1 = d1 - a1;
+  const uint32_t nx = a1 - a0, ny = b1 - b0;
+  {
+    E tmp[LR2];
+#pragma unroll
+    for (int j = 0; j < LR2; ++j) {
+      const uint32_t i = threadIdx.x + j * LNT;
+      const E* src = i < nx ? X + a0 + i : Y + b0 + (i - nx);
+      if (i < nx + ny) tmp[j] = ldg_elem(src);
+    }
+#pragma unroll
+    for (int j = 0; j < LR2; ++j) {
+      const uint32_t i = threadIdx.x + j * LNT;
+      if (i < nx + ny) {
+        sk[pad<LPS>(i)] = tmp[j].k;
+        si[pad<LPS>(i)] = tmp[j].i;
+      }
+    }
+  }
+  __syncthreads();
+  nx_out = nx;
+  auto before = [](uint64_t x, uint64_t y) { return LE ? x <= y : x < y; };
+  const int dd = threadIdx.x * LR2;
+  const int tot = (int)(nx + ny);
+  int cnt = 0;
+  if (dd < tot) {
+    const int NX = (int)nx, NY = (int)ny;
+    int lo = dd > NY ? dd - NY : 0, hi = dd < NX ? dd : NX;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (before(sk[pad<LPS>(mid)], sk[pad<LPS>(NX + dd - 1 - mid)])) lo = mid + 1; else hi = mid;
+    }
+    int ia = lo, ib = dd - lo;
+    const int lastX = max(NX - 1, 0), lastY = NX + max(NY - 1, 0);
+    uint64_t xa = sk[pad<LPS>(min(ia, lastX))], yv = sk[pad<LPS>(min(NX + ib, lastY))];
+    cnt = min(LR2, tot - dd);
+#pragma unroll
+    for (int r = 0; r < LR2; ++r) {
+      const bool takeA = (ib >= NY) || (ia < NX && before(xa, yv));
+      vk[r] = takeA ? xa : yv;
+      vi[r] = si[pad<LPS>(takeA ? min(ia, lastX) : min(NX + ib, lastY))];
+      srcB[r] = !takeA;
+      ia += takeA;
+      ib += !takeA;
+      const uint64_t nv = sk[pad<LPS>(takeA ? min(ia, lastX) : min(NX + ib, lastY))];
+      xa = takeA ? nv : xa;
+      yv = takeA ? yv : nv;
+    }
+  }
+  return cnt;
+}
+
 // merge-path split of diagonal d over X[0,lx) and Y[0,ly) under `before(x, y)`
 template <typename E, typename Before>
 __device__ __forceinline__ uint32_t merge_split(const E* X, uint32_t lx, const E* Y, uint32_t ly, uint32_t d,
@@ -562,32 +631,51 @@ __global__ void __launch_bounds__(LNT) ml_merge_pass(LargeGeom L, const Elem<typ
   const uint32_t ly = y0 < k ? min(run, k - y0) : 0;
   const uint32_t d0 = p0 - x0;
   const uint32_t d1 = min(d0 + LQ, lx + ly);
-  auto before = [](const E& a, const E& c) { return E::less(a, c); };
-  E v[LR2];
   bool srcB[LR2];
   uint32_t nx;
   const uint2 sp = splits[(row * L.nb + b) * L.mtiles + t];
-  const int cnt = merge_tile(s, in + base + x0, in + base + y0, d0, d1, sp, before, v, srcB, nx);
-  __syncthreads();
   const int dd = threadIdx.x * LR2;
+  if constexpr (kSoa<U, KO>) {
+    uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
+    uint32_t* si = reinterpret_cast<uint32_t*>(sk + LQ + (LQ >> LPS) + 1);
+    uint64_t vk[LR2];
+    uint32_t vi[LR2];
+    const int cnt = merge_tile_soa<false>(sk, si, in + base + x0, in + base + y0, d0, d1, sp, vk, vi, srcB, nx);
+    __syncthreads();
 #pragma unroll
-  for (int r = 0; r < LR2; ++r)
-    if (r < cnt) s[pad<LPS>(dd + r)] = v[r];
-  __syncthreads();
-  E* o = out + base + x0 + d0;
-  for (uint32_t i = threadIdx.x; i < d1 - d0; i += LNT) o[i] = s[pad<LPS>(i)];
+    for (int r = 0; r < LR2; ++r)
+      if (r < cnt) {
+        sk[pad<LPS>(dd + r)] = vk[r];
+        si[pad<LPS>(dd + r)] = vi[r];
+      }
+    __syncthreads();
+    Elem<uint64_t>* o = reinterpret_cast<Elem<uint64_t>*>(out + base + x0 + d0);
+    for (uint32_t i = threadIdx.x; i < d1 - d0; i += LNT) store_elem(o + i, sk[pad<LPS>(i)], si[pad<LPS>(i)]);
+  } else {
+    auto before = [](const E& a, const E& c) { return E::less(a, c); };
+    E v[LR2];
+    const int cnt = merge_tile(s, in + base + x0, in + base + y0, d0, d1, sp, before, v, srcB, nx);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < LR2; ++r)
+      if (r < cnt) s[pad<LPS>(dd + r)] = v[r];
+    __syncthreads();
+    E* o = out + base + x0 + d0;
+    for (uint32_t i = threadIdx.x; i < d1 - d0; i += LNT) o[i] = s[pad<LPS>(i)];
+  }
 }
 
 // ---- phase 2a: merge each pair (A = block u, B = block u+1) + live counts -------------
 template <int DT>
-__global__ void __launch_bounds__(LNT, 4) ml_unit_merge(LargeGeom L, const Elem<typename Traits<DT>::U>* S,
+__global__ void __launch_bounds__(LNT, sizeof(typename Traits<DT>::U) == 8 ? 3 : 4) ml_unit_merge(LargeGeom L, const Elem<typename Traits<DT>::U>* S,
                                                      typename Traits<DT>::U* mk, uint32_t* org, uint2* rab,
                                                      uint32_t* live, const uint2* splits) {
   using U = typename Traits<DT>::U;
   using E = Elem<U>;
+  constexpr bool SOA = kSoa<U, true>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   E* s = reinterpret_cast<E*>(smem_raw);                                     // merge tile
-  uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw + sizeof(E) * (LQ + (LQ >> LPS) + 1));  // [4][2][C]
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw + merge_tile_bytes<U, SOA>());  // [4][2][C]
   const uint64_t row = blockIdx.y;
   const uint64_t u = blockIdx.x / L.tiles2;
   const uint32_t t = blockIdx.x % L.tiles2;
@@ -598,26 +686,40 @@ __global__ void __launch_bounds__(LNT, 4) ml_unit_merge(LargeGeom L, const Elem<
   const uint32_t d0 = t * LQ, d1 = min(d0 + LQ, L.nq);
   const uint32_t C = L.C;
   for (uint32_t i = threadIdx.x; i < 8 * C; i += LNT) hist[i] = 0;
-  auto before = [](const E& a, const E& c) { return a.key() <= c.key(); };  // A first on key ties
-  E v[LR2];
+  U vk[LR2];
+  uint32_t vi[LR2];
   bool srcB[LR2];
   uint32_t nx;
   const uint2 sp = splits[(row * L.g.units + u) * L.tiles2 + t];
-  const int cnt = merge_tile(s, A, B, d0, d1, sp, before, v, srcB, nx);
+  int cnt;
+  if constexpr (SOA) {
+    uint64_t* tk = reinterpret_cast<uint64_t*>(smem_raw);
+    uint32_t* ti = reinterpret_cast<uint32_t*>(tk + LQ + (LQ >> LPS) + 1);
+    cnt = merge_tile_soa<true>(tk, ti, A, B, d0, d1, sp, vk, vi, srcB, nx);  // A first on key ties
+  } else {
+    auto before = [](const E& a, const E& c) { return a.key() <= c.key(); };  // A first on key ties
+    E v[LR2];
+    cnt = merge_tile(s, A, B, d0, d1, sp, before, v, srcB, nx);
+#pragma unroll
+    for (int r = 0; r < LR2; ++r) {
+      vk[r] = v[r].key();
+      vi[r] = v[r].idx();
+    }
+  }
   const int dd = threadIdx.x * LR2;
   uint2* ro = rab + ug * (uint64_t)L.C * L.CL;
   __syncthreads();
   // staging: keys, then origins, both padded (pad<LPS>): a thread's LR2 consecutive slots
   // would otherwise put every other lane on the same bank (16-way conflicts)
-  static_assert((sizeof(U) + 4) * (LQ + (LQ >> LPS)) <= merge_tile_smem<U>(), "staging fits the merge tile");
+  static_assert((sizeof(U) + 4) * (LQ + (LQ >> LPS)) <= merge_tile_bytes<U, SOA>(), "staging fits the merge tile");
   U* sk = reinterpret_cast<U*>(s);
   uint32_t* so = reinterpret_cast<uint32_t*>(sk + LQ + (LQ >> LPS));
 #pragma unroll
   for (int r = 0; r < LR2; ++r) {
     if (r < cnt) {
       const uint32_t q = d0 + dd + r;
-      const uint32_t idx = v[r].idx();
-      sk[pad<LPS>(dd + r)] = v[r].key();
+      const uint32_t idx = vi[r];
+      sk[pad<LPS>(dd + r)] = vk[r];
       so[pad<LPS>(dd + r)] = idx | (srcB[r] ? 0x80000000u : 0u);
       uint2* slot = ro + (uint64_t)(idx & (L.CL - 1)) * C + (idx >> L.CLshift);  // transposed [t][c]
       MF_ASSERT(idx < k && q < L.nq && (idx >> L.CLshift) < C);
