@@ -764,24 +764,25 @@ __global__ void __launch_bounds__(LNT, sizeof(typename Traits<DT>::U) == 8 ? 3 :
   }
 }
 
-// live bits of merged positions [32w, 32w+32) just before step i (output i)
+// live bits of merged positions [32w, 32w+32) just before step i (output i).
+// org = idx | isB << 31, and a position is live iff (A and idx >= i) or (B and idx < i),
+// which is exactly "org - i has bit 31 clear": for A, org - i = idx - i underflows iff
+// idx < i; for B, org - i = 2^31 + (idx - i) stays below 2^31 iff idx < i.  One subtract
+// and one shift-or per position; positions past 2k are masked off.
 __device__ __forceinline__ uint32_t live_word(const uint32_t* og, uint32_t w, uint32_t i, uint32_t nq) {
-  uint32_t bits = 0;
+  uint32_t dead = 0;
   const uint4* v4 = reinterpret_cast<const uint4*>(og + w * 32);
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
+  for (int j = 7; j >= 0; --j) {
     const uint4 v = __ldg(v4 + j);
-    const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int l = 0; l < 4; ++l) {
-      const uint32_t q = w * 32 + j * 4 + l;
-      const uint32_t idx = vv[l] & 0x7FFFFFFFu;
-      const bool isB = vv[l] >> 31;
-      const bool lv = q < nq && (isB ? idx < i : idx >= i);
-      bits |= (uint32_t)lv << (j * 4 + l);
-    }
+    dead = (dead << 1) | ((v.w - i) >> 31);
+    dead = (dead << 1) | ((v.z - i) >> 31);
+    dead = (dead << 1) | ((v.y - i) >> 31);
+    dead = (dead << 1) | ((v.x - i) >> 31);
   }
-  return bits;
+  const uint32_t q0 = w * 32;
+  const uint32_t valid = q0 + 32 <= nq ? 0xFFFFFFFFu : (q0 < nq ? (1u << (nq - q0)) - 1u : 0u);
+  return ~dead & valid;
 }
 
 // ---- phase 2c: chunked walk -----------------------------------------------------------
