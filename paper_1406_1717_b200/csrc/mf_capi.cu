@@ -522,7 +522,7 @@ mf_status mf_median_filter_rows(mf_context* ctx, mf_dtype dtype, const void* x, 
     }
     if (!ctx->pool) {
       const unsigned hc = std::max(2u, std::thread::hardware_concurrency());
-      ctx->pool = new CopyPool((int)std::min(15u, hc - 1));
+      ctx->pool = new CopyPool((int)std::min(15u, hc / 2));
     }
     hin = static_cast<char*>(ctx->hstage);
     hout = hin + slots * in_slot;
