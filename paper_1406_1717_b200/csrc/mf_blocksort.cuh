@@ -42,10 +42,6 @@ struct SyncTeam {
   }
 };
 
-#ifndef MF_MERGE_SENT
-#define MF_MERGE_SENT 1  // sentinel-terminated merge steps for 8-byte elements (c5 -1.3 %; 16-byte elements
-                         // keep the bounds tests: their full compare costs more, c1 +13 % measured)
-#endif
 template <typename E, int R, int PS, typename Sync>
 __device__ __forceinline__ void merge_levels_s(E* s, int b0, int tid, int run0, int run_end, E (&v)[R], Sync sync) {
 #pragma unroll 1
@@ -58,31 +54,9 @@ __device__ __forceinline__ void merge_levels_s(E* s, int b0, int tid, int run0, 
     int lo = d > run ? d - run : 0, hi = d < run ? d : run;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if ((MF_MERGE_SENT && sizeof(E) == 8) ? E::less_full(s[pad<PS>(xb + mid)], s[pad<PS>(yb0 + d - 1 - mid)])
-                        : E::less(s[pad<PS>(xb + mid)], s[pad<PS>(yb0 + d - 1 - mid)]))
-        lo = mid + 1;
-      else
-        hi = mid;
+      if (E::less(s[pad<PS>(xb + mid)], s[pad<PS>(yb0 + d - 1 - mid)])) lo = mid + 1; else hi = mid;
     }
     int ia = lo, ib = d - lo;
-    if constexpr (MF_MERGE_SENT && sizeof(E) == 8) {
-    // exhausted sides read as the sentinel, which follows every element in the full (key,
-    // index) order: one full compare per step, no bounds tests.  (The element after a run
-    // is the next run's head or the slot past the tile, always inside the buffer.)
-    E xa = ia < run ? s[pad<PS>(xb + ia)] : E::sentinel();
-    E yv = ib < run ? s[pad<PS>(yb0 + ib)] : E::sentinel();
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const bool takeA = E::less_full(xa, yv);
-      v[r] = E::select(takeA, xa, yv);
-      ia += takeA;
-      ib += !takeA;
-      E nv = s[pad<PS>(takeA ? xb + ia : yb0 + ib)];
-      nv = E::select((takeA ? ia : ib) < run, nv, E::sentinel());
-      xa = E::select(takeA, nv, xa);
-      yv = E::select(takeA, yv, nv);
-    }
-    } else {
     E xa = s[pad<PS>(xb + min(ia, run - 1))], yv = s[pad<PS>(yb0 + min(ib, run - 1))];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -95,7 +69,6 @@ __device__ __forceinline__ void merge_levels_s(E* s, int b0, int tid, int run0, 
       const E nv = s[pad<PS>(nidx)];
       xa = E::select(takeA, nv, xa);
       yv = E::select(takeA, yv, nv);
-    }
     }
     sync();
 #pragma unroll

@@ -71,7 +71,12 @@ struct MediumCfg {
   static constexpr int BL = WP > 1 ? MF_BL_TEAM : MF_BL_WARP;
   // padded element index: blocked per-lane writes hit distinct banks (8-byte elements);
   // the key sort scatters, so its slots are unpadded (the merge walks byte addresses)
-  static constexpr int PS = KS ? 30 : pad_shift<RS>();
+#ifndef MF_KS_PAD
+#define MF_KS_PAD 0  // 1: key-sorted slots padded one element per 16, so the lanes' merge cursors (16 elements
+                     // apart at R = 32) hit distinct banks.  Measured neutral: k = 1023 -1 %, k = 255 / 101 / 63
+                     // +0.8 / +1.2 / +1.1 % (the padded cursor arithmetic costs what the conflicts did)
+#endif
+  static constexpr int PS = KS ? (MF_KS_PAD ? 4 : 30) : pad_shift<RS>();
   static constexpr int SLOT = BS + (BS >> PS) + 1;
   static constexpr size_t sz_sorted = (sizeof(E) * SLOT * (W + 1) + 15) / 16 * 16;
   // merged pos -> key (MK), or -> (isB, sorted pos) where the keys would cost occupancy
@@ -186,8 +191,9 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
     const uint32_t offA = (uint32_t)(reinterpret_cast<const unsigned char*>(A) - reinterpret_cast<const unsigned char*>(ring));
     const uint32_t offB = (uint32_t)(reinterpret_cast<const unsigned char*>(B) - reinterpret_cast<const unsigned char*>(ring));
     const int K = (int)k;
-    const bool exact = (B[K].v & 1ull) != 0;
+    const bool exact = (B[pad<PS>(K)].v & 1ull) != 0;
     uint16_t* rab16 = reinterpret_cast<uint16_t*>(rab);
+    auto padk = [](uint32_t p) -> uint32_t { return p + (p >> PS); };  // slot of sorted position p
     auto run = [&](auto ex) -> uint32_t {
       constexpr bool EX = decltype(ex)::value;
       auto le = [&](uint2 a, uint2 b) -> bool {
@@ -220,21 +226,23 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
           const uint32_t dj = d + j * PLC;
           const bool act = lo[j] < hi[j];
           const uint32_t mid = (lo[j] + hi[j]) >> 1;
-          const bool g = le(at(offA + 8 * (act ? mid : 0u)), at(offB + 8 * (act ? dj - 1 - mid : 0u)));
+          const bool g = le(at(offA + 8 * padk(act ? mid : 0u)), at(offB + 8 * padk(act ? dj - 1 - mid : 0u)));
           lo[j] = act && g ? mid + 1 : lo[j];
           hi[j] = act && !g ? mid : hi[j];
         }
       }
-      const uint32_t limA = offA + 8 * K;
+      const uint32_t limA = offA + 8 * padk(K);
       uint32_t relA[NC], relB[NC], bit[NC], am = 0;
+      uint32_t ia[NC], ib[NC];                  // cursors (sorted positions) of the padded path
       uint2 ea[NC], eb[NC];
 #pragma unroll
       for (int j = 0; j < NC; ++j) {
         const uint32_t dj = d + j * PLC;
-        uint32_t ia = lo[j], ib = dj - lo[j];
-        if (dj >= nq) ia = ib = K;               // chains past the pair: both sides exhausted
-        relA[j] = offA + 8 * ia;
-        relB[j] = offB + 8 * ib;
+        ia[j] = lo[j];
+        ib[j] = dj - lo[j];
+        if (dj >= nq) ia[j] = ib[j] = K;         // chains past the pair: both sides exhausted
+        relA[j] = offA + 8 * padk(ia[j]);
+        relB[j] = offB + 8 * padk(ib[j]);
         ea[j] = at(relA[j]);
         eb[j] = at(relB[j]);
         bit[j] = 1u << (bo + j * PLC);
@@ -256,10 +264,20 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
           rab16[2 * ri + (takeA ? 0 : 1)] = (uint16_t)q;
           am |= takeA ? bit[j] : 0u;
           bit[j] <<= 1;
-          relA[j] += takeA ? 8u : 0u;
-          relB[j] += takeA ? 0u : 8u;
-          // only A can pass its sentinel (ties go to A); B never passes it
-          const uint2 nv = at(takeA ? min(relA[j], limA) : relB[j]);
+          uint2 nv;
+          if constexpr (PS < 30) {  // padded slots: the next address from the advanced cursor
+            ia[j] += takeA ? 1u : 0u;
+            ib[j] += takeA ? 0u : 1u;
+            // only A can pass its sentinel (ties go to A); B never passes it
+            const uint32_t a = (takeA ? offA : offB) + 8 * padk(takeA ? min(ia[j], (uint32_t)K) : ib[j]);
+            relA[j] = takeA ? a : relA[j];
+            relB[j] = takeA ? relB[j] : a;
+            nv = at(a);
+          } else {
+            relA[j] += takeA ? 8u : 0u;
+            relB[j] += takeA ? 0u : 8u;
+            nv = at(takeA ? min(relA[j], limA) : relB[j]);
+          }
           ea[j] = takeA ? nv : ea[j];
           eb[j] = takeA ? eb[j] : nv;
         }
