@@ -450,12 +450,13 @@ __device__ __forceinline__ int merge_tile(E* s, const E* X, const E* Y, uint32_t
   const uint32_t a0 = sp.x, a1 = sp.y;   // merge-path splits, precomputed by ml_partition_*
   const uint32_t b0 = d0 - a0, b1 = d1 - a1;
   const uint32_t nx = a1 - a0, ny = b1 - b0;
+  const uint32_t yoff = (uint32_t)(Y - X);  // Y follows X in the same buffer (runs / blocks)
   {  // stage the tile's inputs: all LR2 global loads in flight before the shared stores
     E tmp[LR2];
 #pragma unroll
     for (int j = 0; j < LR2; ++j) {
       const uint32_t i = threadIdx.x + j * LNT;
-      const E* src = i < nx ? X + a0 + i : Y + b0 + (i - nx);
+      const E* src = X + (i < nx ? a0 + i : yoff + b0 + (i - nx));  // 32-bit offset, one 64-bit add
       if (i < nx + ny) tmp[j] = ldg_elem(src);
     }
 #pragma unroll
@@ -505,12 +506,13 @@ __device__ __forceinline__ int merge_tile_soa(uint64_t* sk, uint32_t* si, const 
   const uint32_t a0 = sp.x, a1 = sp.y;
   const uint32_t b0 = d0 - a0, b1 = d1 - a1;
   const uint32_t nx = a1 - a0, ny = b1 - b0;
+  const uint32_t yoff = (uint32_t)(Y - X);  // Y follows X in the same buffer (runs / blocks)
   {
     E tmp[LR2];
 #pragma unroll
     for (int j = 0; j < LR2; ++j) {
       const uint32_t i = threadIdx.x + j * LNT;
-      const E* src = i < nx ? X + a0 + i : Y + b0 + (i - nx);
+      const E* src = X + (i < nx ? a0 + i : yoff + b0 + (i - nx));  // 32-bit offset, one 64-bit add
       if (i < nx + ny) tmp[j] = ldg_elem(src);
     }
 #pragma unroll
@@ -721,7 +723,7 @@ __global__ void __launch_bounds__(LNT, sizeof(typename Traits<DT>::U) == 8 ? 3 :
       const uint32_t idx = vi[r];
       sk[pad<LPS>(dd + r)] = vk[r];
       so[pad<LPS>(dd + r)] = idx | (srcB[r] ? 0x80000000u : 0u);
-      uint2* slot = ro + (uint64_t)(idx & (L.CL - 1)) * C + (idx >> L.CLshift);  // transposed [t][c]
+      uint2* slot = ro + ((idx & (L.CL - 1)) * C + (idx >> L.CLshift));  // transposed [t][c] (< C*CL: 32-bit)
       MF_ASSERT(idx < k && q < L.nq && (idx >> L.CLshift) < C);
       if (srcB[r]) slot->y = q; else slot->x = q;
       const uint32_t sw = (dd + r) >> 10;                   // superword within the tile
