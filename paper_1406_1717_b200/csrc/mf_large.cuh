@@ -37,8 +37,11 @@ constexpr size_t merge_tile_smem() { return sizeof(Elem<U>) * (LQ + (LQ >> LPS) 
 #ifndef MF_TS_SOA
 #define MF_TS_SOA 1
 #endif
+#ifndef MF_SOA32
+#define MF_SOA32 0  // 1: 32-bit keys too (4-byte key compares in the merge tiles): measured c5 +0.6 %
+#endif
 template <typename U, bool KO>
-constexpr bool kSoa = MF_TS_SOA && KO && sizeof(U) == 8;
+constexpr bool kSoa = MF_TS_SOA && KO && (sizeof(U) == 8 || MF_SOA32);
 template <typename U, bool SOA>
 constexpr size_t merge_tile_bytes() {
   return (SOA ? sizeof(U) + sizeof(uint32_t) : sizeof(Elem<U>)) * (LQ + (LQ >> LPS) + 1);
@@ -499,9 +502,9 @@ __device__ __forceinline__ int merge_tile(E* s, const E* X, const E* Y, uint32_t
 // merge_tile over struct-of-arrays shared tiles (64-bit keys): keys in sk, indices in si,
 // key compares only (LE: x goes first on ties, else y does); the taken element's index is
 // loaded off the dependency chain.
-template <bool LE, typename E>
-__device__ __forceinline__ int merge_tile_soa(uint64_t* sk, uint32_t* si, const E* X, const E* Y, uint32_t d0,
-                                              uint32_t d1, uint2 sp, uint64_t (&vk)[LR2], uint32_t (&vi)[LR2],
+template <bool LE, typename U, typename E>
+__device__ __forceinline__ int merge_tile_soa(U* sk, uint32_t* si, const E* X, const E* Y, uint32_t d0,
+                                              uint32_t d1, uint2 sp, U (&vk)[LR2], uint32_t (&vi)[LR2],
                                               bool (&srcB)[LR2], uint32_t& nx_out) {
   const uint32_t a0 = sp.x, a1 = sp.y;
   const uint32_t b0 = d0 - a0, b1 = d1 - a1;
@@ -519,14 +522,14 @@ __device__ __forceinline__ int merge_tile_soa(uint64_t* sk, uint32_t* si, const 
     for (int j = 0; j < LR2; ++j) {
       const uint32_t i = threadIdx.x + j * LNT;
       if (i < nx + ny) {
-        sk[pad<LPS>(i)] = tmp[j].k;
-        si[pad<LPS>(i)] = tmp[j].i;
+        sk[pad<LPS>(i)] = tmp[j].key();
+        si[pad<LPS>(i)] = tmp[j].idx();
       }
     }
   }
   __syncthreads();
   nx_out = nx;
-  auto before = [](uint64_t x, uint64_t y) { return LE ? x <= y : x < y; };
+  auto before = [](U x, U y) { return LE ? x <= y : x < y; };
   const int dd = threadIdx.x * LR2;
   const int tot = (int)(nx + ny);
   int cnt = 0;
@@ -539,7 +542,7 @@ __device__ __forceinline__ int merge_tile_soa(uint64_t* sk, uint32_t* si, const 
     }
     int ia = lo, ib = dd - lo;
     const int lastX = max(NX - 1, 0), lastY = NX + max(NY - 1, 0);
-    uint64_t xa = sk[pad<LPS>(min(ia, lastX))], yv = sk[pad<LPS>(min(NX + ib, lastY))];
+    U xa = sk[pad<LPS>(min(ia, lastX))], yv = sk[pad<LPS>(min(NX + ib, lastY))];
     cnt = min(LR2, tot - dd);
 #pragma unroll
     for (int r = 0; r < LR2; ++r) {
@@ -549,7 +552,7 @@ __device__ __forceinline__ int merge_tile_soa(uint64_t* sk, uint32_t* si, const 
       srcB[r] = !takeA;
       ia += takeA;
       ib += !takeA;
-      const uint64_t nv = sk[pad<LPS>(takeA ? min(ia, lastX) : min(NX + ib, lastY))];
+      const U nv = sk[pad<LPS>(takeA ? min(ia, lastX) : min(NX + ib, lastY))];
       xa = takeA ? nv : xa;
       yv = takeA ? yv : nv;
     }
@@ -638,9 +641,9 @@ __global__ void __launch_bounds__(LNT) ml_merge_pass(LargeGeom L, const Elem<typ
   const uint2 sp = splits[(row * L.nb + b) * L.mtiles + t];
   const int dd = threadIdx.x * LR2;
   if constexpr (kSoa<U, KO>) {
-    uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
+    U* sk = reinterpret_cast<U*>(smem_raw);
     uint32_t* si = reinterpret_cast<uint32_t*>(sk + LQ + (LQ >> LPS) + 1);
-    uint64_t vk[LR2];
+    U vk[LR2];
     uint32_t vi[LR2];
     const int cnt = merge_tile_soa<false>(sk, si, in + base + x0, in + base + y0, d0, d1, sp, vk, vi, srcB, nx);
     __syncthreads();
@@ -651,7 +654,7 @@ __global__ void __launch_bounds__(LNT) ml_merge_pass(LargeGeom L, const Elem<typ
         si[pad<LPS>(dd + r)] = vi[r];
       }
     __syncthreads();
-    Elem<uint64_t>* o = reinterpret_cast<Elem<uint64_t>*>(out + base + x0 + d0);
+    Elem<U>* o = reinterpret_cast<Elem<U>*>(out + base + x0 + d0);
     for (uint32_t i = threadIdx.x; i < d1 - d0; i += LNT) store_elem(o + i, sk[pad<LPS>(i)], si[pad<LPS>(i)]);
   } else {
     auto before = [](const E& a, const E& c) { return E::less(a, c); };
@@ -695,7 +698,7 @@ __global__ void __launch_bounds__(LNT, sizeof(typename Traits<DT>::U) == 8 ? 3 :
   const uint2 sp = splits[(row * L.g.units + u) * L.tiles2 + t];
   int cnt;
   if constexpr (SOA) {
-    uint64_t* tk = reinterpret_cast<uint64_t*>(smem_raw);
+    U* tk = reinterpret_cast<U*>(smem_raw);
     uint32_t* ti = reinterpret_cast<uint32_t*>(tk + LQ + (LQ >> LPS) + 1);
     cnt = merge_tile_soa<true>(tk, ti, A, B, d0, d1, sp, vk, vi, srcB, nx);  // A first on key ties
   } else {
