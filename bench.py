@@ -281,6 +281,16 @@ def run_ours(args):
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(f"{cfg}_k{kdom}")
 
+    # per-phase device times of one extra (untimed) call per k (MF_OPT_PROFILE events)
+    phases = None
+    if rank == 0 and not args.no_check:
+        ctx.profile(True)
+        phases = {}
+        for k, xv, _n in jobs:
+            call(k, xv)
+            phases[str(k)] = [[name, ms] for name, ms in ctx.last_phases()]
+        ctx.profile(False)
+
     # fold_checksum of every k's global output (chained over ranks), against the golden
     checks = None
     if not args.no_check:
@@ -339,6 +349,7 @@ def run_ours(args):
                        "per_k_samples_per_s": {str(k): [j[2] for j in jobs if j[0] == k][0] * world / (per_k_ms[k] / 1e3)
                                                for k in ks}},
             "checksums": checks,
+            "phases": phases,
             "gather": gather,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel_k": kdom,

@@ -47,8 +47,9 @@ typedef enum { MF_I32 = 0, MF_I64 = 1, MF_F32 = 2, MF_F64 = 3 } mf_dtype;
 typedef enum { MF_CLASS_AUTO = -1, MF_CLASS_SMALL = 0, MF_CLASS_MEDIUM = 1, MF_CLASS_LARGE = 2 } mf_class;
 
 typedef enum {
-  MF_OPT_FORCE_CLASS = 0,    /* value: mf_class; a forced class must support k */
-  MF_OPT_PIPELINE_CHUNK = 1  /* value: largest host-pipeline chunk in samples (0 = default 2^23) */
+  MF_OPT_FORCE_CLASS = 0,     /* value: mf_class; a forced class must support k */
+  MF_OPT_PIPELINE_CHUNK = 1,  /* value: largest host-pipeline chunk in samples (0 = default 2^23) */
+  MF_OPT_PROFILE = 2          /* value 1: device entries record per-phase CUDA events (mf_context_last_phases) */
 } mf_option;
 
 typedef struct mf_context mf_context;
@@ -78,6 +79,12 @@ void mf_context_destroy(mf_context* ctx);
 mf_status mf_context_set_option(mf_context* ctx, mf_option opt, long value);
 /* Number of kernels the last call on this context launched. */
 uint64_t mf_context_last_launches(const mf_context* ctx);
+/* Per-phase device times of the last device-entry call made with MF_OPT_PROFILE on: phase
+ * names (static strings, e.g. "large: tile sort", "large: merge passes", "large: pair merge",
+ * "large: walk") and milliseconds between consecutive phase marks; waits for the call to
+ * finish.  Returns the number of phases (0 if none were recorded); fills at most `cap`.
+ * Every call also emits NVTX ranges / marks (entries and phases) for nsys-style tools. */
+int mf_context_last_phases(mf_context* ctx, const char** names, float* ms, int cap);
 
 /* ---- host-buffer entry: the literal drop-in for median_filter<T> (filter.hpp:149-155).
  * x: n host samples; y: host buffer with capacity y_cap >= max(0, n-k+1); *y_len gets the

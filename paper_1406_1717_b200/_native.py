@@ -18,12 +18,14 @@ MF_I32, MF_I64, MF_F32, MF_F64 = 0, 1, 2, 3
 MF_CLASS_AUTO, MF_CLASS_SMALL, MF_CLASS_MEDIUM, MF_CLASS_LARGE = -1, 0, 1, 2
 MF_OPT_FORCE_CLASS = 0
 MF_OPT_PIPELINE_CHUNK = 1
+MF_OPT_PROFILE = 2
 MF_GEN_UNIFORM_F32, MF_GEN_UNIFORM_F64, MF_GEN_MOD_I32 = 0, 1, 2
 
 # Every symbol include/medfilt_gpu.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "mf_status_string", "mf_error_message", "mf_window_spec", "mf_kernel_class",
-    "mf_context_create", "mf_context_create_multi", "mf_context_devices", "mf_context_destroy", "mf_context_set_option", "mf_context_last_launches",
+    "mf_context_create", "mf_context_create_multi", "mf_context_devices", "mf_context_destroy",
+    "mf_context_set_option", "mf_context_last_launches", "mf_context_last_phases",
     "mf_median_filter", "mf_median_filter_device", "mf_median_filter_rows",
     "mf_median_filter_rows_device", "mf_block_sort_device", "mf_generate_device",
     "mf_generate_trend_f64_host", "mf_fold_checksum",
@@ -64,6 +66,8 @@ def lib() -> C.CDLL:
         L.mf_context_set_option.argtypes = [vp, C.c_int, C.c_long]
         L.mf_context_last_launches.argtypes = [vp]
         L.mf_context_last_launches.restype = u64
+        L.mf_context_last_phases.argtypes = [vp, C.POINTER(C.c_char_p), C.POINTER(C.c_float), C.c_int]
+        L.mf_context_last_phases.restype = C.c_int
         L.mf_median_filter.argtypes = [vp, C.c_int, vp, sz, sz, vp, sz, C.POINTER(sz)]
         L.mf_median_filter_device.argtypes = [vp, C.c_int, vp, sz, sz, vp, vp]
         L.mf_median_filter_rows.argtypes = [vp, C.c_int, vp, sz, sz, sz, sz, vp, sz]

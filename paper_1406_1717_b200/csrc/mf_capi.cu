@@ -14,6 +14,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/medfilt_gpu.h"
 #include "mf_launch.h"
 
@@ -115,6 +117,9 @@ struct mf_context {
   // streams, so concurrent large-k calls on two streams never overlap on ws)
   cudaEvent_t ws_ev = nullptr;
   bool ws_ev_recorded = false;
+  // MF_OPT_PROFILE: the device entries record a CUDA event at every phase mark
+  bool profile = false;
+  mf::PhaseTrace trace;
   // pageable host buffers: pinned staging slots and the copy pool (created on first use)
   void* hstage = nullptr;
   size_t hstage_bytes = 0;
@@ -199,8 +204,10 @@ mf_status run_rows(mf_context* ctx, mf_dtype dtype, const void* d_x, size_t rows
   g.keep = keep; g.units = (keep + k - 1) / k; g.rows = (uint32_t)rows;
   cudaError_t e;
   if (cls == MF_CLASS_SMALL) {
+    mf::phase_mark(s, k == 3 ? "small: k=3 selection" : "small: fused sort + walk");
     e = mf::launch_small(dtype, g, s, &ctx->launches);
   } else if (cls == MF_CLASS_MEDIUM) {
+    mf::phase_mark(s, "medium: fused sort + merge + walk");
     e = mf::launch_medium(dtype, g, s, &ctx->launches);
   } else {
     // the large-k kernels put rows on grid.y (<= 65535): run row groups
@@ -330,6 +337,8 @@ void mf_context_destroy(mf_context* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->ws_ev) cudaEventDestroy(ctx->ws_ev);
+  for (cudaEvent_t ev : ctx->trace.ev)
+    if (ev) cudaEventDestroy(ev);
   if (ctx->hstage) cudaFreeHost(ctx->hstage);
   delete ctx->pool;
   if (ctx->io) cudaFree(ctx->io);
@@ -355,6 +364,11 @@ mf_status mf_context_set_option(mf_context* ctx, mf_option opt, long value) {
     ctx->force_class = (int)value;
     return MF_OK;
   }
+  if (opt == MF_OPT_PROFILE) {
+    if (value != 0 && value != 1) return MF_BAD_ARG;
+    ctx->profile = value != 0;
+    return MF_OK;
+  }
   if (opt == MF_OPT_PIPELINE_CHUNK) {
     if (value < 0) return MF_BAD_ARG;
     ctx->chunk_elems = value == 0 ? size_t(1) << 23 : std::max<size_t>(1024, (size_t)value);
@@ -365,12 +379,40 @@ mf_status mf_context_set_option(mf_context* ctx, mf_option opt, long value) {
 
 uint64_t mf_context_last_launches(const mf_context* ctx) { return ctx ? ctx->launches : 0; }
 
+int mf_context_last_phases(mf_context* ctx, const char** names, float* ms, int cap) {
+  if (!ctx || !ctx->subs.empty()) return 0;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  const mf::PhaseTrace& t = ctx->trace;
+  if (t.n == 0 || !t.ev[t.n]) return 0;
+  if (cudaSetDevice(ctx->device) != cudaSuccess || cudaEventSynchronize(t.ev[t.n]) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  for (int i = 0; i < t.n && i < cap; ++i) {
+    if (names) names[i] = t.name[i];
+    if (ms && cudaEventElapsedTime(&ms[i], t.ev[i], t.ev[i + 1]) != cudaSuccess) {
+      cudaGetLastError();
+      ms[i] = -1.0f;
+    }
+  }
+  return t.n;
+}
+
 mf_status mf_median_filter_rows_device(mf_context* ctx, mf_dtype dtype, const void* d_x, size_t rows,
                                        size_t n, size_t ld_x, size_t k, void* d_y, size_t ld_y,
                                        void* stream) {
   if (!ctx || !ctx->subs.empty()) return MF_BAD_ARG;  // device pointers live on one device
   std::lock_guard<std::mutex> lock(ctx->mu);
-  return run_rows(ctx, dtype, d_x, rows, n, ld_x, k, d_y, ld_y, pick(ctx, stream));
+  nvtxRangePushA("mf_median_filter_rows_device");
+  cudaStream_t s = pick(ctx, stream);
+  if (ctx->profile) mf::phase_begin(&ctx->trace);
+  const mf_status st = run_rows(ctx, dtype, d_x, rows, n, ld_x, k, d_y, ld_y, s);
+  if (ctx->profile) {
+    if (cudaSetDevice(ctx->device) == cudaSuccess) mf::phase_end(s);
+    if (st != MF_OK) ctx->trace.n = 0;
+  }
+  nvtxRangePop();
+  return st;
 }
 
 mf_status mf_median_filter_device(mf_context* ctx, mf_dtype dtype, const void* d_x, size_t n, size_t k,
@@ -466,6 +508,10 @@ mf_status mf_median_filter_rows(mf_context* ctx, mf_dtype dtype, const void* x, 
   ctx->launches = 0;
   if (keep == 0 || rows == 0) return MF_OK;
   if (!x || !y || ld_x < n || ld_y < keep) return MF_BAD_ARG;
+  struct Range {  // NVTX range around the host entry (free without a tool attached)
+    Range() { nvtxRangePushA("mf_median_filter_rows (host buffers)"); }
+    ~Range() { nvtxRangePop(); }
+  } range;
   if (!ctx->subs.empty()) return multi_rows(ctx, dtype, x, rows, n, ld_x, k, y, ld_y, keep);
   if (cudaSetDevice(ctx->device) != cudaSuccess) return MF_NO_DEVICE;
 #ifndef MF_PIPE_SLOTS

@@ -99,6 +99,7 @@ cudaError_t sort_blocks(const LargeGeom& L, unsigned char* ws, const Layout<DT>&
   cudaError_t e = configure<DT>(L);
   if (e != cudaSuccess) return e;
   E* bufs[2] = {reinterpret_cast<E*>(ws + lay.off_s0), reinterpret_cast<E*>(ws + lay.off_s1)};
+  phase_mark(s, "large: tile sort");
 #if MF_TILE_RADIX
   static_assert(TileRadix<U>::TS == TileSort<U>::TS, "tile size is shared with the merge passes");
   ml_tile_radix<DT><<<dim3((unsigned)(L.nb * L.tiles), L.g.rows), TileRadix<U>::NT, TileRadix<U>::smem, s>>>(
@@ -114,6 +115,7 @@ cudaError_t sort_blocks(const LargeGeom& L, unsigned char* ws, const Layout<DT>&
   int cur = 0;
   uint2* splits = reinterpret_cast<uint2*>(ws + lay.off_split);
   const uint64_t ptiles = (uint64_t)L.g.rows * L.nb * L.mtiles;
+  if ((uint64_t)L.TS < L.g.k) phase_mark(s, "large: merge passes");
   for (uint64_t run = L.TS; run < L.g.k; run *= 2) {
     ml_partition_pass<DT, KO><<<(unsigned)((ptiles + 127) / 128), 128, 0, s>>>(L, bufs[cur], splits, (uint32_t)run,
                                                                          ptiles);
@@ -144,11 +146,13 @@ cudaError_t run_large_dt(const Geom& g, void* wsv, size_t ws_bytes, cudaStream_t
   const size_t um = merge_tile_bytes<U, kSoa<U, true>>() + sizeof(uint32_t) * 8 * L.C;
   uint2* splits = reinterpret_cast<uint2*>(ws + lay.off_split);
   const uint64_t utiles = (uint64_t)g.rows * g.units * L.tiles2;
+  phase_mark(s, "large: pair merge");
   ml_partition_units<DT><<<(unsigned)((utiles + 127) / 128), 128, 0, s>>>(L, sorted, splits, utiles);
   ml_unit_merge<DT><<<dim3((unsigned)(g.units * L.tiles2), g.rows), LNT, um, s>>>(L, sorted, mk, org, rab, live,
                                                                                   splits);
   *launches += 2;
   const uint64_t nchunks = nu * L.C;
+  phase_mark(s, "large: walk");
   ml_walk<DT><<<(unsigned)((nchunks + LNT - 1) / LNT), LNT, sizeof(U) * 32 * 9 * (LNT / 32), s>>>(
       L, mk, org, rab, live, nchunks);
   ++*launches;

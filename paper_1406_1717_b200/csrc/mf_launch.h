@@ -17,6 +17,22 @@ struct LaunchInfo {
 };
 cudaError_t kernel_setup(const void* func, size_t smem, int threads, LaunchInfo* out);
 
+// Phase tracing (mf_setup.cu).  Launchers mark the start of each phase of a filter call
+// (e.g. the large-k pipeline's tile sort, merge passes, pair merge and walk): an NVTX mark
+// always (free without a tool attached), and -- while a context with MF_OPT_PROFILE runs a
+// call on this thread -- a CUDA event on the launching stream, from which the C ABI
+// reports per-phase device times (mf_context_last_phases).
+struct PhaseTrace {
+  static constexpr int kMax = 64;
+  cudaEvent_t ev[kMax + 1] = {};
+  const char* name[kMax] = {};
+  int n = 0;          // phases marked by the last call
+  bool open = false;  // a call is recording
+};
+void phase_begin(PhaseTrace* t);                 // this thread's calls record into t
+void phase_mark(cudaStream_t s, const char* name);
+void phase_end(cudaStream_t s);                  // closes the last phase, stops recording
+
 // Largest k each fused class handles (per key width).
 constexpr uint32_t kSmallMaxK = 31;        // 64-bit keys
 #ifndef MF_SMALL_MAXK32

@@ -10,6 +10,8 @@
 #include <mutex>
 #include <tuple>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "mf_launch.h"
 
 namespace mf {
@@ -55,6 +57,35 @@ cudaError_t kernel_setup(const void* func, size_t smem, int threads, LaunchInfo*
   }
   if (out) *out = LaunchInfo{en.sms, res};
   return cudaSuccess;
+}
+
+namespace {
+thread_local PhaseTrace* t_trace = nullptr;
+}
+
+void phase_begin(PhaseTrace* t) {
+  t_trace = t;
+  if (!t) return;
+  t->n = 0;
+  t->open = true;
+}
+
+void phase_mark(cudaStream_t s, const char* name) {
+  nvtxMarkA(name);
+  PhaseTrace* t = t_trace;
+  if (!t || !t->open || t->n >= PhaseTrace::kMax) return;
+  if (!t->ev[t->n] && cudaEventCreate(&t->ev[t->n]) != cudaSuccess) return;
+  if (cudaEventRecord(t->ev[t->n], s) != cudaSuccess) return;
+  t->name[t->n++] = name;
+}
+
+void phase_end(cudaStream_t s) {
+  PhaseTrace* t = t_trace;
+  t_trace = nullptr;
+  if (!t || !t->open) return;
+  t->open = false;
+  if (!t->ev[t->n] && cudaEventCreate(&t->ev[t->n]) != cudaSuccess) { t->n = 0; return; }
+  if (cudaEventRecord(t->ev[t->n], s) != cudaSuccess) t->n = 0;
 }
 
 }  // namespace mf

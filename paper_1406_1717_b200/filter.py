@@ -125,6 +125,18 @@ class Context:
     def last_launches(self) -> int:
         return int(N.lib().mf_context_last_launches(self._h))
 
+    def profile(self, on: bool = True) -> None:
+        """Record per-phase CUDA events in the device entries (read with last_phases)."""
+        _check(N.lib().mf_context_set_option(self._h, N.MF_OPT_PROFILE, int(bool(on))))
+
+    def last_phases(self) -> list[tuple[str, float]]:
+        """(phase name, device ms) of the last device-entry call made with profile() on."""
+        cap = 64
+        names = (C.c_char_p * cap)()
+        ms = (C.c_float * cap)()
+        n = int(N.lib().mf_context_last_phases(self._h, names, ms, cap))
+        return [(names[i].decode(), float(ms[i])) for i in range(min(n, cap))]
+
     def __del__(self):
         try:
             if self._h:
