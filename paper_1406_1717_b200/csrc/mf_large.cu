@@ -4,9 +4,17 @@
 
 #include "mf_launch.h"
 #include "mf_large.cuh"
+#include "mf_pair.cuh"
 
 #ifndef MF_LARGE_KEYORD
 #define MF_LARGE_KEYORD 1  // the filter's block sort compares keys only (the phase API never does)
+#endif
+#ifndef MF_PAIR
+#define MF_PAIR 0  // 1: fused shared-memory pair phase (ml_pair, mf_pair.cuh) for 1023 < k <= 16383.
+                   // Bit-exact (c4 golden, checked build) but slower: c4 11.59 ms against 8.32 ms for
+                   // ml_unit_merge + ml_walk.  Its ~180 KB of pair state leaves one CTA (8 warps) per
+                   // SM, so the phases (merge rounds with exposed staging latency, 64 walkers) run
+                   // serialised at 7 % warps active (profiles/r02_pair_experiment.txt).
 #endif
 #ifndef MF_TILE_RADIX
 #define MF_TILE_RADIX 0  // 1: LSD radix tile sort, 0: comparison network + merge levels
@@ -148,6 +156,16 @@ cudaError_t run_large_dt(const Geom& g, void* wsv, size_t ws_bytes, cudaStream_t
   const uint64_t utiles = (uint64_t)g.rows * g.units * L.tiles2;
   phase_mark(s, "large: pair merge");
   ml_partition_units<DT><<<(unsigned)((utiles + 127) / 128), 128, 0, s>>>(L, sorted, splits, utiles);
+  if (MF_PAIR && g.k <= kPairMaxK) {
+    const PairGeom P = pair_plan(g.k, merge_tile_bytes<U, kSoa<U, true>>());
+    if (P.smem <= 227u * 1024u) {
+      if ((e = kernel_setup((const void*)ml_pair<DT>, P.smem, 0, nullptr)) != cudaSuccess) return e;
+      phase_mark(s, "large: fused pair merge + walk");
+      ml_pair<DT><<<dim3((unsigned)g.units, g.rows), LNT, P.smem, s>>>(L, P, sorted, splits);
+      *launches += 2;
+      return cudaGetLastError();
+    }
+  }
   ml_unit_merge<DT><<<dim3((unsigned)(g.units * L.tiles2), g.rows), LNT, um, s>>>(L, sorted, mk, org, rab, live,
                                                                                   splits);
   *launches += 2;
