@@ -140,6 +140,55 @@ __device__ __forceinline__ void warp_sort_regs(E (&v)[R], E* s, int b0, uint32_t
   merge_levels<E, R, PS, false>(s, b0, lane, R << BL, 32 * R, v);
 }
 
+// Merge-path levels over the SoA arrays (runs run0, 2*run0, ... < run_end); thread `tid`
+// produces outputs [j*R, j*R + R) of its merged run pair.  Key compares are strict in both
+// the search and the steps, so the lanes' ranges tile each merged run exactly.
+// With `aos` set, the last level writes its outputs as 16-byte {key, index} elements into
+// `aos` (which may overlap sk/si: every read of the level precedes the write-back barrier).
+template <int R, int PS, typename Sync, typename EA = KElem64>
+__device__ __forceinline__ void merge_levels_soa(uint64_t* sk, uint32_t* si, int b0, int tid, int run0, int run_end,
+                                                 uint64_t (&vk)[R], uint32_t (&vi)[R], Sync sync,
+                                                 EA* aos = nullptr) {
+#pragma unroll 1
+  for (int run = run0; run < run_end; run *= 2) {
+    const int gl = (2 * run) / R;                // threads per merged run
+    const int j = tid & (gl - 1);
+    const int xb = b0 + (tid / gl) * (2 * run);  // X = [xb, xb+run), Y = [xb+run, xb+2run)
+    const int yb0 = xb + run;
+    const int d = j * R;
+    int lo = d > run ? d - run : 0, hi = d < run ? d : run;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (sk[pad<PS>(xb + mid)] < sk[pad<PS>(yb0 + d - 1 - mid)]) lo = mid + 1; else hi = mid;
+    }
+    int ia = lo, ib = d - lo;
+    uint64_t xa = sk[pad<PS>(xb + min(ia, run - 1))], yv = sk[pad<PS>(yb0 + min(ib, run - 1))];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const bool takeA = (ib >= run) || (ia < run && xa < yv);
+      vk[r] = takeA ? xa : yv;
+      vi[r] = si[pad<PS>(takeA ? xb + ia : yb0 + ib)];   // off the chain
+      ia += takeA;
+      ib += !takeA;
+      const uint64_t nv = sk[pad<PS>(takeA ? xb + min(ia, run - 1) : yb0 + min(ib, run - 1))];
+      xa = takeA ? nv : xa;
+      yv = takeA ? yv : nv;
+    }
+    sync();
+    if (aos && 2 * run >= run_end) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) aos[pad<PS>(xb + d + r)] = EA::make(vk[r], vi[r]);
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        sk[pad<PS>(xb + d + r)] = vk[r];
+        si[pad<PS>(xb + d + r)] = vi[r];
+      }
+    }
+    sync();
+  }
+}
+
 // Warp-wide stable compaction of the elements with idx < k to the front of sb[0, NS).
 // Needed after a key-ordered sort (KElem) when the block holds samples whose key is the
 // all-ones padding key (real maxima or the reference's +INF padding, filter.hpp:28-36):
@@ -179,7 +228,31 @@ __device__ __forceinline__ void team_sort_raw(E* sb, const typename Traits<DT>::
     v[r] = E::make(Traits<DT>::enc(raw[r]), e);
     maxkey |= e < k && raw[r] == padv;
   }
-  warp_sort_regs<E, RS, PS, BL>(v, sb, sub * 32 * RS, lane);
+#ifndef MF_MED_SOA64
+#define MF_MED_SOA64 1  // one-warp 64-bit key sorts merge through SoA scratch (keys, indices) inside the slot
+#endif
+  if constexpr (MF_MED_SOA64 && WP == 1 && std::is_same_v<E, KElem64> && RS < 32) {
+    // register network, then the merge levels over struct-of-arrays scratch laid in the slot's
+    // own bytes (12 bytes per element fit in its 16); the last level writes the slot's
+    // {key, index} elements
+    constexpr int NSL = 32 * RS + ((32 * RS) >> PS) + 1;
+    static_assert(12 * NSL <= 16 * NSL, "SoA scratch fits the slot");
+    sort_regs<RS>(v);
+    uint64_t* sk = reinterpret_cast<uint64_t*>(sb);
+    uint32_t* si = reinterpret_cast<uint32_t*>(sk + NSL);
+#pragma unroll
+    for (int r = 0; r < RS; ++r) {
+      const int p = pad<PS>((int)(lane * RS + r));
+      sk[p] = v[r].k;
+      si[p] = v[r].i;
+    }
+    __syncwarp();
+    uint64_t vk[RS];
+    uint32_t vi[RS];
+    merge_levels_soa<RS, PS>(sk, si, 0, (int)lane, RS, 32 * RS, vk, vi, SyncWarp{}, sb);
+  } else {
+    warp_sort_regs<E, RS, PS, BL>(v, sb, sub * 32 * RS, lane);
+  }
   if constexpr (WP > 1) {
     maxkey = bar.any(maxkey);
     merge_levels_s<E, RS, PS>(sb, 0, sub * 32 + lane, 32 * RS, 32 * RS * WP, v, bar);

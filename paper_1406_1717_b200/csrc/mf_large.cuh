@@ -206,47 +206,6 @@ struct TileSoa {
   static constexpr size_t smem = (sizeof(uint64_t) + sizeof(uint32_t)) * NSLOT + sizeof(uint32_t) * (LNT / 32);
 };
 
-// Merge-path levels over the SoA arrays (runs run0, 2*run0, ... < run_end); thread `tid`
-// produces outputs [j*R, j*R + R) of its merged run pair.  Key compares are strict in both
-// the search and the steps, so the lanes' ranges tile each merged run exactly.
-template <int R, int PS, typename Sync>
-__device__ __forceinline__ void merge_levels_soa(uint64_t* sk, uint32_t* si, int b0, int tid, int run0, int run_end,
-                                                 uint64_t (&vk)[R], uint32_t (&vi)[R], Sync sync) {
-#pragma unroll 1
-  for (int run = run0; run < run_end; run *= 2) {
-    const int gl = (2 * run) / R;                // threads per merged run
-    const int j = tid & (gl - 1);
-    const int xb = b0 + (tid / gl) * (2 * run);  // X = [xb, xb+run), Y = [xb+run, xb+2run)
-    const int yb0 = xb + run;
-    const int d = j * R;
-    int lo = d > run ? d - run : 0, hi = d < run ? d : run;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (sk[pad<PS>(xb + mid)] < sk[pad<PS>(yb0 + d - 1 - mid)]) lo = mid + 1; else hi = mid;
-    }
-    int ia = lo, ib = d - lo;
-    uint64_t xa = sk[pad<PS>(xb + min(ia, run - 1))], yv = sk[pad<PS>(yb0 + min(ib, run - 1))];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const bool takeA = (ib >= run) || (ia < run && xa < yv);
-      vk[r] = takeA ? xa : yv;
-      vi[r] = si[pad<PS>(takeA ? xb + ia : yb0 + ib)];   // off the chain
-      ia += takeA;
-      ib += !takeA;
-      const uint64_t nv = sk[pad<PS>(takeA ? xb + min(ia, run - 1) : yb0 + min(ib, run - 1))];
-      xa = takeA ? nv : xa;
-      yv = takeA ? yv : nv;
-    }
-    sync();
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      sk[pad<PS>(xb + d + r)] = vk[r];
-      si[pad<PS>(xb + d + r)] = vi[r];
-    }
-    sync();
-  }
-}
-
 template <int DT>
 __global__ void __launch_bounds__(LNT, MF_TS_SOA_MINB) ml_tile_sort_soa(LargeGeom L, Elem<uint64_t>* out) {
   using Tr = Traits<DT>;
