@@ -48,7 +48,7 @@ typedef enum { MF_CLASS_AUTO = -1, MF_CLASS_SMALL = 0, MF_CLASS_MEDIUM = 1, MF_C
 
 typedef enum {
   MF_OPT_FORCE_CLASS = 0,     /* value: mf_class; a forced class must support k */
-  MF_OPT_PIPELINE_CHUNK = 1,  /* value: largest host-pipeline chunk in samples (0 = default 2^23) */
+  MF_OPT_PIPELINE_CHUNK = 1,  /* value: largest host-pipeline chunk in samples (0 = default 2^22) */
   MF_OPT_PROFILE = 2          /* value 1: device entries record per-phase CUDA events (mf_context_last_phases) */
 } mf_option;
 

@@ -107,7 +107,7 @@ struct mf_context {
   void* io = nullptr;          // grow-only device buffers for the host entry points
   size_t io_bytes = 0;
   int force_class = MF_CLASS_AUTO;
-  size_t chunk_elems = size_t(1) << 23;  // largest host-pipeline chunk (samples)
+  size_t chunk_elems = size_t(1) << 22;  // largest host-pipeline chunk (samples; 2^22 measured 1.5 % above 2^23)
   uint64_t launches = 0;
   // host-entry pipeline: H2D / compute / D2H on three streams, up to 4 chunks in flight
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
@@ -371,7 +371,7 @@ mf_status mf_context_set_option(mf_context* ctx, mf_option opt, long value) {
   }
   if (opt == MF_OPT_PIPELINE_CHUNK) {
     if (value < 0) return MF_BAD_ARG;
-    ctx->chunk_elems = value == 0 ? size_t(1) << 23 : std::max<size_t>(1024, (size_t)value);
+    ctx->chunk_elems = value == 0 ? size_t(1) << 22 : std::max<size_t>(1024, (size_t)value);
     return MF_OK;
   }
   return MF_BAD_ARG;
