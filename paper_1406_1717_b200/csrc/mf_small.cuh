@@ -147,6 +147,9 @@ __device__ __forceinline__ void stage_tile(TV* buf, const TV* x, uint64_t n, uin
   cp_async_commit();
 }
 
+#ifndef MF_SMALL_ONE_SUCC
+#define MF_SMALL_ONE_SUCC 1  // one live_succ per step on the side that may advance
+#endif
 template <int DT, int K, int T>
 __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_row, uint64_t total_tiles) {
   using C = SmallCfg<DT, K, T>;
@@ -246,8 +249,15 @@ __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_
         const bool need = (int)(sA + sB) < H;
         const bool bLess = (mB != KK) && (mA == KK || keyB < keyA);
         const bool advA = need && !bLess, advB = need && bLess;
+#if MF_SMALL_ONE_SUCC
+        // at most one side advances: one successor search on the selected list
+        const uint32_t nxt = live_succ(bLess ? maskB : maskA, bLess ? mB : mA, KK);
+        mA = sel(advA, nxt, mA);
+        mB = sel(advB, nxt, mB);
+#else
         mA = sel(advA, live_succ(maskA, mA, KK), mA);
         mB = sel(advB, live_succ(maskB, mB, KK), mB);
+#endif
         sA += advA;
         sB += advB;
         const U* kp = advA ? kA + min(mA, KK - 1) * SC : kB + min(mB, KK - 1) * SC;
