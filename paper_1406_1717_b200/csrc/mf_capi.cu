@@ -538,7 +538,9 @@ mf_status mf_median_filter_rows(mf_context* ctx, mf_dtype dtype, const void* x, 
   // and the D2H of the last (the parts nothing overlaps) are small.
   const bool by_rows = rows > 1;
   const size_t total = by_rows ? rows : keep;  // units to cut
-  const size_t cmax = by_rows ? std::max<size_t>(1, kChunkElems / n) : std::min(keep, std::max<size_t>(kChunkElems, 16 * k));
+  // large windows take chunks of at least 128 windows: every chunk re-sorts its blocks and pays the
+  // large-k pipeline's launches, so a 2^22-sample chunk at k = 100001 would cost c5 a third of its e2e
+  const size_t cmax = by_rows ? std::max<size_t>(1, kChunkElems / n) : std::min(keep, std::max<size_t>(kChunkElems, 128 * k));
   const size_t cmin = std::max<size_t>(by_rows ? 1 : std::min(cmax, 16 * k), cmax / MF_PIPE_RAMP);
   std::vector<size_t> sizes = chunk_schedule(total, cmin, cmax);
   const size_t nchunks = sizes.size();
