@@ -38,6 +38,12 @@ namespace mf {
 #define MF_MEDIUM_KEYORD_MAXR 16  // largest R sorted with key-ordered elements (R = 32: measured slower)
 #endif
 
+#ifndef MF_WALK_WT
+#define MF_WALK_WT 1  // the walk writes every Delete/Undelete through to the rows (two atomics per step).
+                      // 0 (rows kept at their chunk-start value, a word rebuilt by replaying the chunk's
+                      // steps when the cursor enters it) measured slower: k = 1023 1.41 -> 1.84 ms, k = 255
+                      // 0.98 -> 1.09 ms -- the cursor changes words far more often than once a chunk
+#endif
 #ifndef MF_ROWS_PAD
 #define MF_ROWS_PAD 1
 #endif
@@ -456,10 +462,14 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
               const uint32_t a = ab & 0xFFFF, b = ab >> 16;
               MF_ASSERT(a < nq && b < nq && tl < (uint32_t)CH);
               const uint32_t ba = 1u << (a & 31), bb = 1u << (b & 31);
-              // Delete(A, i-1) and Undelete(B, i-1), written through to the row in shared
-              // memory (fire-and-forget atomics, no divergence) and to the cached cursor word
+              // Delete(A, i-1) and Undelete(B, i-1) on the cached cursor word; with MF_WALK_WT
+              // also written through to the row (fire-and-forget atomics), else the row keeps its
+              // chunk-start value and a word the cursor moves into is rebuilt from it and the
+              // chunk's earlier steps (rare)
+#if MF_WALK_WT
               atomicAnd(&rows[row_addr<CH, C::NWP>(tl, a >> 5)], ~ba);
               atomicOr(&rows[row_addr<CH, C::NWP>(tl, b >> 5)], bb);
+#endif
               cb = sel((a >> 5) == cw, cb & ~ba, cb);
               cb = sel((b >> 5) == cw, cb | bb, cb);
               // the cursor moves up when the deletion is at or below it and the insertion above
@@ -475,6 +485,15 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
                   cw += dir;
                   MF_ASSERT(cw < nw);
                   cb = rows[row_addr<CH, C::NWP>(tl, cw)];
+#if !MF_WALK_WT
+#pragma unroll 1
+                  for (int tt = 1; tt <= t; ++tt) {  // replay this chunk's steps so far on word cw
+                    const uint32_t ab2 = rab[(tt - 1) * CH + tl];
+                    const uint32_t a2 = ab2 & 0xFFFF, b2 = ab2 >> 16;
+                    cb = sel((a2 >> 5) == cw, cb & ~(1u << (a2 & 31)), cb);
+                    cb = sel((b2 >> 5) == cw, cb | (1u << (b2 & 31)), cb);
+                  }
+#endif
                   m = cb;
                 } while (m == 0);
               }
