@@ -167,3 +167,15 @@ def test_repeat_determinism_under_concurrency(oracle, k):
     torch.cuda.synchronize()
     for rep, o in enumerate(outs):
         assert np.array_equal(bits(o.cpu().numpy()), want), f"k={k} repetition {rep}"
+
+
+def test_multi_device_shard_counts(multi, oracle):
+    """Fewer rows than devices, one row, and signals just above and below the minimum
+    shard size all give the single-device result."""
+    rng = np.random.default_rng(12)
+    xr = rng.integers(-9, 9, size=(1, 5000)).astype(np.int64)
+    assert np.array_equal(mf.median_filter_rows(xr, 101, ctx=multi)[0], oracle.median_filter(xr[0], 101))
+    for n in ((1 << 21) + 100 - 1, (1 << 21) + 300):     # keep below / above 2 x 2^20 outputs
+        x = rng.standard_normal(n).astype(np.float32)
+        assert np.array_equal(bits(mf.median_filter(x, 201, ctx=multi)),
+                              bits(mf.median_filter(x, 201, ctx=mf.Context.get(0))))
