@@ -57,7 +57,10 @@ __device__ __forceinline__ void merge_levels_s(E* s, int b0, int tid, int run0, 
       if (E::less(s[pad<PS>(xb + mid)], s[pad<PS>(yb0 + d - 1 - mid)])) lo = mid + 1; else hi = mid;
     }
     int ia = lo, ib = d - lo;
-    E xa = s[pad<PS>(xb + min(ia, run - 1))], yv = s[pad<PS>(yb0 + min(ib, run - 1))];
+    // An exhausted side's cursor reads the element after its run: Y's head for X, the next
+    // run pair's head (or the tile's spare slot) for Y -- always inside the buffer, and never
+    // taken (the bounds tests decide), so no clamps are needed.
+    E xa = s[pad<PS>(xb + ia)], yv = s[pad<PS>(yb0 + ib)];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       // branch-free step: one shared load refills whichever side was consumed
@@ -65,8 +68,7 @@ __device__ __forceinline__ void merge_levels_s(E* s, int b0, int tid, int run0, 
       v[r] = E::select(takeA, xa, yv);
       ia += takeA;
       ib += !takeA;
-      const int nidx = takeA ? xb + min(ia, run - 1) : yb0 + min(ib, run - 1);
-      const E nv = s[pad<PS>(nidx)];
+      const E nv = s[pad<PS>(takeA ? xb + ia : yb0 + ib)];
       xa = E::select(takeA, nv, xa);
       yv = E::select(takeA, yv, nv);
     }
@@ -162,7 +164,7 @@ __device__ __forceinline__ void merge_levels_soa(uint64_t* sk, uint32_t* si, int
       if (sk[pad<PS>(xb + mid)] < sk[pad<PS>(yb0 + d - 1 - mid)]) lo = mid + 1; else hi = mid;
     }
     int ia = lo, ib = d - lo;
-    uint64_t xa = sk[pad<PS>(xb + min(ia, run - 1))], yv = sk[pad<PS>(yb0 + min(ib, run - 1))];
+    uint64_t xa = sk[pad<PS>(xb + ia)], yv = sk[pad<PS>(yb0 + ib)];  // unclamped: see merge_levels_s
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const bool takeA = (ib >= run) || (ia < run && xa < yv);
@@ -170,7 +172,7 @@ __device__ __forceinline__ void merge_levels_soa(uint64_t* sk, uint32_t* si, int
       vi[r] = si[pad<PS>(takeA ? xb + ia : yb0 + ib)];   // off the chain
       ia += takeA;
       ib += !takeA;
-      const uint64_t nv = sk[pad<PS>(takeA ? xb + min(ia, run - 1) : yb0 + min(ib, run - 1))];
+      const uint64_t nv = sk[pad<PS>(takeA ? xb + ia : yb0 + ib)];
       xa = takeA ? nv : xa;
       yv = takeA ? yv : nv;
     }

@@ -440,8 +440,8 @@ __device__ __forceinline__ int merge_tile(E* s, const E* X, const E* Y, uint32_t
       if (before(s[pad<LPS>(mid)], s[pad<LPS>(NX + dd - 1 - mid)])) lo = mid + 1; else hi = mid;
     }
     int ia = lo, ib = dd - lo;
-    const int lastX = max(NX - 1, 0), lastY = NX + max(NY - 1, 0);
-    E xa = s[pad<LPS>(min(ia, lastX))], yv = s[pad<LPS>(min(NX + ib, lastY))];
+    // unclamped cursors: past X reads Y's head, past Y the slot after the tile (never taken)
+    E xa = s[pad<LPS>(ia)], yv = s[pad<LPS>(NX + ib)];
     cnt = min(LR2, tot - dd);
 #pragma unroll
     for (int r = 0; r < LR2; ++r) {
@@ -450,7 +450,7 @@ __device__ __forceinline__ int merge_tile(E* s, const E* X, const E* Y, uint32_t
       srcB[r] = !takeA;
       ia += takeA;
       ib += !takeA;
-      const E nv = s[pad<LPS>(takeA ? min(ia, lastX) : min(NX + ib, lastY))];
+      const E nv = s[pad<LPS>(takeA ? ia : NX + ib)];
       xa = E::select(takeA, nv, xa);
       yv = E::select(takeA, yv, nv);
     }
@@ -500,18 +500,17 @@ __device__ __forceinline__ int merge_tile_soa(U* sk, uint32_t* si, const E* X, c
       if (before(sk[pad<LPS>(mid)], sk[pad<LPS>(NX + dd - 1 - mid)])) lo = mid + 1; else hi = mid;
     }
     int ia = lo, ib = dd - lo;
-    const int lastX = max(NX - 1, 0), lastY = NX + max(NY - 1, 0);
-    U xa = sk[pad<LPS>(min(ia, lastX))], yv = sk[pad<LPS>(min(NX + ib, lastY))];
+    U xa = sk[pad<LPS>(ia)], yv = sk[pad<LPS>(NX + ib)];  // unclamped, as in merge_tile
     cnt = min(LR2, tot - dd);
 #pragma unroll
     for (int r = 0; r < LR2; ++r) {
       const bool takeA = (ib >= NY) || (ia < NX && before(xa, yv));
       vk[r] = takeA ? xa : yv;
-      vi[r] = si[pad<LPS>(takeA ? min(ia, lastX) : min(NX + ib, lastY))];
+      vi[r] = si[pad<LPS>(takeA ? ia : NX + ib)];
       srcB[r] = !takeA;
       ia += takeA;
       ib += !takeA;
-      const U nv = sk[pad<LPS>(takeA ? min(ia, lastX) : min(NX + ib, lastY))];
+      const U nv = sk[pad<LPS>(takeA ? ia : NX + ib)];
       xa = takeA ? nv : xa;
       yv = takeA ? yv : nv;
     }
