@@ -51,9 +51,12 @@ constexpr size_t merge_tile_bytes() {
 template <typename U> struct TileSortCfg;
 template <> struct TileSortCfg<uint32_t> { static constexpr int R = 32; };
 template <> struct TileSortCfg<uint64_t> { static constexpr int R = 16; };
+#ifndef MF_TS_PS
+#define MF_TS_PS 0  // pad shift of the tile sort's shared tile (0: pad_shift<R>())
+#endif
 template <typename U> struct TileSort {
   static constexpr int R = TileSortCfg<U>::R;
-  static constexpr int PS = pad_shift<R>();
+  static constexpr int PS = MF_TS_PS ? MF_TS_PS : pad_shift<R>();
   static constexpr int TS = 8 * 32 * R;
   static constexpr size_t smem = sizeof(Elem<U>) * (TS + (TS >> PS) + 1) + sizeof(uint32_t) * (LNT / 32);
 };
