@@ -71,7 +71,10 @@ mf_status mf_context_create(int device, mf_context** out);
  * output ranges with a (k-1)-sample input halo, a batch by whole row groups (SURVEY.md
  * §8(e)); each device's D2H lands directly at its offset of the caller's output.  Outputs
  * are identical to a single-device call.  Device-pointer entries reject a multi-device
- * context with MF_BAD_ARG (a device pointer lives on one device). */
+ * context only if the pointers are not device memory: with device pointers (on any one
+ * "home" device), the device entries copy each shard peer to peer (peer access is enabled
+ * here where the devices allow it: NVLink on a B200 box), filter it on its device and copy
+ * its outputs back to the home buffer -- stream-ordered on the caller's stream. */
 mf_status mf_context_create_multi(const int* devices, int ndev, mf_context** out);
 /* Number of devices of ctx; writes up to `cap` device ids to `devices` (may be NULL). */
 int mf_context_devices(const mf_context* ctx, int* devices, int cap);

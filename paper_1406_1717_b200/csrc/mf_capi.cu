@@ -312,6 +312,16 @@ mf_status mf_context_create_multi(const int* devices, int ndev, mf_context** out
     }
     ctx->subs.push_back(sub);
   }
+  // direct NVLink copies between the devices for the device-resident multi-device entry
+  for (int i = 0; i < ndev; ++i)
+    for (int j = 0; j < ndev; ++j) {
+      int can = 0;
+      if (devices[i] == devices[j] || cudaDeviceCanAccessPeer(&can, devices[i], devices[j]) != cudaSuccess || !can)
+        continue;
+      cudaSetDevice(devices[i]);
+      if (cudaDeviceEnablePeerAccess(devices[j], 0) != cudaSuccess) cudaGetLastError();  // already enabled
+    }
+  cudaSetDevice(devices[0]);
   *out = ctx;
   return MF_OK;
 }
@@ -398,10 +408,114 @@ int mf_context_last_phases(mf_context* ctx, const char** names, float* ms, int c
   return t.n;
 }
 
+// Device-resident multi-device entry (the cudaMemcpyPeer variant): the
+// signal (or batch) lives on one "home" device.  Each sub-context's device takes a shard --
+// halo'd output ranges of a signal, row groups of a batch -- copied peer to peer (NVLink
+// when peer access is on), filters it on its own stream, and copies its outputs back to the
+// home buffer at their offset; the home device's own shard is filtered in place.  Stream
+// ordered: every device waits on an event recorded on the caller's stream, and the caller's
+// stream waits on every device's completion event, so the call returns after enqueueing.
+// Caller holds ctx->mu.
+static mf_status multi_device_rows(mf_context* ctx, mf_dtype dtype, const void* d_x, size_t rows, size_t n,
+                                   size_t ld_x, size_t k, void* d_y, size_t ld_y, size_t keep, cudaStream_t stream) {
+  cudaPointerAttributes pa{};
+  if (cudaPointerGetAttributes(&pa, d_x) != cudaSuccess || pa.type != cudaMemoryTypeDevice) {
+    cudaGetLastError();
+    return MF_BAD_ARG;
+  }
+  const int home = pa.device;
+  const size_t w = dtype_size(dtype), G = ctx->subs.size();
+  struct Part { size_t xo, yo, rows, n, ld_x, ld_y, in_elems, out_elems; };
+  std::vector<Part> parts;
+  if (rows > 1) {
+    const size_t use = std::min(G, rows);
+    for (size_t g = 0; g < use; ++g) {
+      const size_t r0 = rows * g / use, r1 = rows * (g + 1) / use;
+      parts.push_back({r0 * ld_x, r0 * ld_y, r1 - r0, n, ld_x, ld_y, (r1 - r0) * ld_x, (r1 - r0) * ld_y});
+    }
+  } else {
+    const size_t min_out = std::max<size_t>(size_t(1) << 20, 16 * k);
+    const size_t use = std::max<size_t>(1, std::min(G, keep / min_out));
+    for (size_t g = 0; g < use; ++g) {
+      const size_t o0 = keep * g / use, o1 = keep * (g + 1) / use, ni = o1 - o0 + k - 1;
+      parts.push_back({o0, o0, 1, ni, ni, o1 - o0, ni, o1 - o0});
+    }
+  }
+  size_t first_home = parts.size();
+  for (size_t i = 0; i < parts.size(); ++i)
+    if (ctx->subs[i]->device == home) { first_home = i; break; }
+  if (cudaSetDevice(home) != cudaSuccess) return MF_NO_DEVICE;
+  cudaEvent_t start = nullptr;
+  if (cudaEventCreateWithFlags(&start, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventRecord(start, stream) != cudaSuccess)
+    return MF_CUDA_ERROR;
+  std::vector<cudaEvent_t> done(parts.size(), nullptr);
+  mf_status st = MF_OK;
+  uint64_t launches = 0;
+  for (size_t i = 0; i < parts.size() && st == MF_OK; ++i) {
+    mf_context* sub = ctx->subs[i];
+    std::lock_guard<std::mutex> sl(sub->mu);
+    const Part& p = parts[i];
+    if (cudaSetDevice(sub->device) != cudaSuccess) { st = MF_NO_DEVICE; break; }
+    if (cudaStreamWaitEvent(sub->stream, start, 0) != cudaSuccess) { st = MF_CUDA_ERROR; break; }
+    const char* x0 = static_cast<const char*>(d_x) + p.xo * w;
+    char* y0 = static_cast<char*>(d_y) + p.yo * w;
+    if (sub->device == home && i == first_home) {  // the home device's own shard, in place
+      st = run_rows(sub, dtype, x0, p.rows, p.n, p.ld_x, k, y0, p.ld_y, sub->stream);
+    } else {
+      const size_t in_b = (p.in_elems * w + 255) / 256 * 256, out_b = (p.out_elems * w + 255) / 256 * 256;
+      if ((st = grow(&sub->io, &sub->io_bytes, in_b + out_b)) != MF_OK) break;
+      char* sx = static_cast<char*>(sub->io);
+      char* sy = sx + in_b;
+      if (cudaMemcpyPeerAsync(sx, sub->device, x0, home, p.in_elems * w, sub->stream) != cudaSuccess) {
+        st = MF_CUDA_ERROR;
+        break;
+      }
+      st = run_rows(sub, dtype, sx, p.rows, p.n, p.ld_x, k, sy, p.ld_y, sub->stream);
+      // outputs back to their offset; strided rows row by row, so the caller's row gaps stay
+      // untouched, as in the single-device entry
+      const size_t outw = p.rows > 1 ? keep : p.out_elems;
+      for (size_t r = 0; r < p.rows && st == MF_OK; ++r)
+        if (cudaMemcpyPeerAsync(y0 + r * p.ld_y * w, home, sy + r * p.ld_y * w, sub->device,
+                                (p.rows > 1 && p.ld_y == keep) ? p.rows * keep * w : outw * w, sub->stream) != cudaSuccess)
+          st = MF_CUDA_ERROR;
+        else if (p.rows > 1 && p.ld_y == keep)
+          break;  // contiguous rows: one copy
+    }
+    launches += sub->launches;
+    if (st == MF_OK && (cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming) != cudaSuccess ||
+                        cudaEventRecord(done[i], sub->stream) != cudaSuccess))
+      st = MF_CUDA_ERROR;
+  }
+  cudaSetDevice(home);
+  for (cudaEvent_t ev : done)
+    if (ev) {
+      if (cudaStreamWaitEvent(stream, ev, 0) != cudaSuccess && st == MF_OK) st = MF_CUDA_ERROR;
+      cudaEventDestroy(ev);  // released once complete
+    }
+  cudaEventDestroy(start);
+  ctx->launches = launches;
+  return st;
+}
+
 mf_status mf_median_filter_rows_device(mf_context* ctx, mf_dtype dtype, const void* d_x, size_t rows,
                                        size_t n, size_t ld_x, size_t k, void* d_y, size_t ld_y,
                                        void* stream) {
-  if (!ctx || !ctx->subs.empty()) return MF_BAD_ARG;  // device pointers live on one device
+  if (!ctx) return MF_BAD_ARG;
+  if (!ctx->subs.empty()) {  // several devices: peer-copied shards (see multi_device_rows)
+    size_t keep = 0;
+    mf_status st = mf_window_spec(n, k, nullptr, nullptr, &keep);
+    if (st != MF_OK) return st;
+    if (!dtype_ok(dtype)) return MF_BAD_ARG;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    ctx->launches = 0;
+    if (keep == 0 || rows == 0) return MF_OK;
+    if (!d_x || !d_y || ld_x < n || ld_y < keep) return MF_BAD_ARG;
+    nvtxRangePushA("mf_median_filter_rows_device (multi-device)");
+    st = multi_device_rows(ctx, dtype, d_x, rows, n, ld_x, k, d_y, ld_y, keep, pick(ctx, stream));
+    nvtxRangePop();
+    return st;
+  }
   std::lock_guard<std::mutex> lock(ctx->mu);
   nvtxRangePushA("mf_median_filter_rows_device");
   cudaStream_t s = pick(ctx, stream);

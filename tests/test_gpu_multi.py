@@ -69,11 +69,11 @@ def test_multi_device_small_signal_and_errors(multi, oracle):
     assert mf.median_filter(x[:5], 7, ctx=multi).size == 0
     with pytest.raises(mf.InvalidArgument, match="^even window size"):
         mf.median_filter(x, 4, ctx=multi)
-    # device pointers live on one device: the device entries reject a multi context
-    import torch
-    xd = torch.from_numpy(x).cuda()
-    with pytest.raises(ValueError):
-        mf.median_filter_device(xd, 31, ctx=multi)
+    # host memory through a device entry is refused
+    L = N.lib()
+    y = np.empty(x.size, dtype=x.dtype)
+    assert L.mf_median_filter_device(multi.handle, N.MF_I32, C.c_void_p(x.ctypes.data), x.size, 31,
+                                     C.c_void_p(y.ctypes.data), None) == N.MF_BAD_ARG
 
 
 def test_cpp_set_devices_multi():
@@ -179,3 +179,38 @@ def test_multi_device_shard_counts(multi, oracle):
         x = rng.standard_normal(n).astype(np.float32)
         assert np.array_equal(bits(mf.median_filter(x, 201, ctx=multi)),
                               bits(mf.median_filter(x, 201, ctx=mf.Context.get(0))))
+
+
+@pytest.mark.parametrize("k", [3, 31, 255, 1023, 4097])
+def test_multi_device_device_pointers_equal_single(multi, k):
+    """Device-resident input on the multi-device context: shards copied peer to peer (the
+    second listed device copies even when it is the same GPU), filtered on each device and
+    copied back to their offsets, stream-ordered on the caller's stream."""
+    import torch
+    x = mf.generate_device("uniform_f32", 31, (3 << 20) + 77)
+    want = mf.median_filter_device(x, k).cpu().numpy()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        got = mf.median_filter_device(x, k, ctx=multi, stream=s)
+    s.synchronize()
+    assert np.array_equal(bits(got.cpu().numpy()), bits(want))
+
+
+def test_multi_device_device_rows_strided():
+    """Rows on device with row strides wider than the rows: row groups go to the devices
+    and the outputs' row gaps are left untouched."""
+    import torch
+    multi = mf.Context.multi([0, 0, 0])
+    xr = mf.generate_device("mod_i32", 5, 7 * 30_011, mod=16).view(7, 30_011)
+    big = torch.zeros((7, 30_011 + 5), dtype=torch.int32, device="cuda")
+    big[:, :30_011] = xr
+    keep = 30_011 - 255 + 1
+    out = torch.full((7, keep + 9), -1, dtype=torch.int32, device="cuda")
+    L = N.lib()
+    assert L.mf_median_filter_rows_device(multi.handle, N.MF_I32, C.c_void_p(big.data_ptr()), 7, 30_011,
+                                          30_011 + 5, 255, C.c_void_p(out.data_ptr()), keep + 9, None) == 0
+    torch.cuda.synchronize()
+    want = mf.median_filter_rows_device(xr, 255).cpu().numpy()
+    o = out.cpu().numpy()
+    assert np.array_equal(o[:, :keep], want)
+    assert (o[:, keep:] == -1).all()
