@@ -295,8 +295,11 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
     return am;
   };
 
+  // (row, tile-in-row) of the current tile, advanced incrementally (no 64-bit division per tile)
+  uint64_t row = t_begin / tiles_per_row, tr = t_begin % tiles_per_row;
   for (uint64_t t = t_begin; t < t_end; ++t) {
-    const uint64_t row = t / tiles_per_row, tr = t % tiles_per_row;
+    uint64_t nrow = row, ntr = tr + 1;
+    if (ntr == tiles_per_row) { ntr = 0; ++nrow; }
     const uint64_t u0 = tr * W;
     const TV* __restrict__ x = reinterpret_cast<const TV*>(g.x) + row * g.ld_x;
     TV* __restrict__ y = reinterpret_cast<TV*>(g.y) + row * g.ld_y;
@@ -317,7 +320,6 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
     // blocks only: for small R the extra registers cost more occupancy than they hide)
     have_pre = R >= 16 && t + 1 < t_end;
     if (have_pre) {
-      const uint64_t nrow = (t + 1) / tiles_per_row, ntr = (t + 1) % tiles_per_row;
       team_load_block<TV, RS, WP>(pre, reinterpret_cast<const TV*>(g.x) + nrow * g.ld_x, g.n, k,
                                   ntr * W + team + 1, sub, lane);
     }
@@ -503,20 +505,30 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
           }
         }
         team_sync();  // rows are dead: reuse them as the output staging area
+        // a chunk's SR (<= 32, a power of two) outputs share one 32-group, so its padded
+        // staging offset is one base plus the step
+        const uint32_t ob = i0 + (i0 >> 5);
 #pragma unroll
         for (int t = 0; t < SR; ++t)
           if (i0 + t < imax) {
-            check_sptr(&ost[i0 + t + ((i0 + t) >> 5)]);
-            ost[i0 + t + ((i0 + t) >> 5)] = out[t];
+            check_sptr(&ost[ob + t]);
+            ost[ob + t] = out[t];
           }
         team_sync();
-        TV* yo = y + u * k;
+        TV* yo = y + u * k + tl;
         MF_ASSERT(u * k + imax <= g.keep);
-        for (uint32_t i = tl; i < imax; i += TL) yo[i] = Tr::dec(ost[i + (i >> 5)]);
+        // team lane tl stores outputs tl + TL*j: fixed strides, so unrolled loads and stores
+        // take immediate offsets
+        const U* os = ost + tl + (tl >> 5);
+#pragma unroll
+        for (int j = 0; j < RS; ++j)
+          if (tl + (uint32_t)(TL * j) < imax) yo[TL * j] = Tr::dec(os[(TL + WP) * j]);
       }
     }
     prev_row = row;
     prev_tile = tr;
+    row = nrow;
+    tr = ntr;
     __syncthreads();  // the ring slots are reused by the next tile
   }
 }
