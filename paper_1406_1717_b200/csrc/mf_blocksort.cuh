@@ -364,7 +364,9 @@ __device__ __forceinline__ uint32_t lower_bound_keys4(uint32_t s0, uint32_t x) {
 }
 
 #ifndef MF_LB4_MIN
-#define MF_LB4_MIN 1024  // smallest run searched with 4-way steps (measured: k = 1023 1.70 -> 1.64 ms, k = 255 +0.7 %)
+#define MF_LB4_MIN 2048  // smallest run searched with 4-way steps.  Round 1 (latency-bound): 4-way at 1024 keys, k = 1023
+                         // 1.70 -> 1.64 ms.  Round 2: the kernel is bound by shared-memory wavefronts (75 % of peak), and the
+                         // binary search issues 11 loads per key instead of 16: k = 1023 1.335 -> 1.245 ms
 #endif
 template <int N>
 __device__ __forceinline__ uint32_t lower_bound_sel(uint32_t s, uint32_t x) {
@@ -388,28 +390,34 @@ __device__ __forceinline__ void team_sort_keys(KElem32* sb, const typename Trait
                                                uint32_t* cnt) {
   constexpr int NS = 32 * RS;             // keys per warp
   constexpr int SKW = NS + NS / 32;       // padded words per warp
+  constexpr uint32_t BS = WP * NS;
   const uint32_t tl = sub * 32 + lane;
-  {
-    uint4* c4 = reinterpret_cast<uint4*>(cnt);
-    for (uint32_t i = tl; i < (uint32_t)(WP * NS / 4); i += 32 * WP) c4[i] = make_uint4(0, 0, 0, 0);
-  }
   uint32_t key[RS];
   KeyU32 v[RS];
+  bool maxkey = false;                    // a real element (e < k) has the all-ones key
 #pragma unroll
   for (int r = 0; r < RS; ++r) {
     key[r] = Traits<DT>::enc(raw[r]);
     v[r].v = key[r];
+    maxkey |= sub * NS + lane + 32 * r < k && key[r] == 0xFFFFFFFFu;
   }
   sort_regs<RS>(v);
   warp_bitonic_keys<RS, 5>(v, lane);
   uint32_t* mine = sk + sub * SKW;
 #pragma unroll
   for (int r = 0; r < RS; ++r) mine[pad<5>((int)lane * RS + r)] = v[r].v;
-  if constexpr (WP > 1) bar(); else __syncwarp();
+  // `ties`: two equal keys below the all-ones key sit next to each other in the sorted block,
+  // or a real element has the all-ones key (it ties with the slot fillers).  Without ties every
+  // real element's position is its count of smaller keys, and the tie-slot counters are skipped.
+#ifndef MF_TIE_SKIP
+#define MF_TIE_SKIP 1
+#endif
+  bool ties = maxkey || !MF_TIE_SKIP;
   // two warps: one merge-path level joins their runs, so each element searches once
   constexpr bool MERGE = WP == 2 && MF_TEAM_KEYMERGE;
   const uint32_t* srch = sk;
   if constexpr (MERGE) {
+    bar();
     uint32_t* skm = sk + 2 * SKW;
     const uint32_t* X = sk;
     const uint32_t* Y = sk + SKW;
@@ -434,8 +442,25 @@ __device__ __forceinline__ void team_sort_keys(KElem32* sb, const typename Trait
     }
 #pragma unroll
     for (int r = 0; r < RS; ++r) skm[pad<5>(d + r)] = o[r];
+    // (two-warp teams always count tie slots: detecting ties across the merged run measured
+    // slower than the counters it saves, k = 1023 1.318 -> 1.338 ms)
+    ties = true;
     bar();
     srch = skm;
+  } else if constexpr (WP == 1) {
+    const uint32_t nxt = __shfl_down_sync(0xFFFFFFFFu, v[0].v, 1);
+#pragma unroll
+    for (int r = 0; r + 1 < RS; ++r) ties |= v[r].v == v[r + 1].v && v[r].v != 0xFFFFFFFFu;
+    ties |= lane < 31 && v[RS - 1].v == nxt && nxt != 0xFFFFFFFFu;
+    ties = __any_sync(0xFFFFFFFFu, ties);
+    __syncwarp();                           // the stores to `mine` before the searches
+  } else {
+    ties = bar.any(true);                   // separate runs per warp: always count tie slots
+  }
+  if (ties) {
+    uint4* c4 = reinterpret_cast<uint4*>(cnt);
+    for (uint32_t i = tl; i < (uint32_t)(WP * NS / 4); i += 32 * WP) c4[i] = make_uint4(0, 0, 0, 0);
+    if constexpr (WP > 1) bar(); else __syncwarp();
   }
   // shared-window addresses of the sorted runs, tied to the barrier above
   const uint32_t tok = order_token();
@@ -453,21 +478,31 @@ __device__ __forceinline__ void team_sort_keys(KElem32* sb, const typename Trait
   }
   // tie slots and the scatter, branch-free: slot fillers count on cnt[BS-1] (never a real
   // element's rank, which is < k <= BS-1) and write the unused slot position BS
-  constexpr uint32_t BS = WP * NS;
-  bool maxkey = false;
+  if (ties) {
 #pragma unroll
-  for (int r = 0; r < RS; ++r) {
-    const uint32_t e = sub * NS + lane + 32 * r;
-    const bool real = e < k;
-    maxkey |= real && key[r] == 0xFFFFFFFFu;
-    MF_ASSERT(!real || pos[r] < k);
-    check_sptr(&cnt[real ? pos[r] : BS - 1]);
-    const uint32_t t = atomicAdd(&cnt[real ? pos[r] : BS - 1], 1u);
-    uint32_t ri = e;
-    if constexpr (SRr > 0) ri = (e & (SRr - 1)) * CHr + e / SRr;
-    MF_ASSERT(!real || pos[r] + t < k);
-    check_sptr(&sb[pad<PS>((int)(real ? pos[r] + t : BS))]);
-    sb[pad<PS>((int)(real ? pos[r] + t : BS))] = KElem32::make(key[r], ri);
+    for (int r = 0; r < RS; ++r) {
+      const uint32_t e = sub * NS + lane + 32 * r;
+      const bool real = e < k;
+      MF_ASSERT(!real || pos[r] < k);
+      check_sptr(&cnt[real ? pos[r] : BS - 1]);
+      const uint32_t t = atomicAdd(&cnt[real ? pos[r] : BS - 1], 1u);
+      uint32_t ri = e;
+      if constexpr (SRr > 0) ri = (e & (SRr - 1)) * CHr + e / SRr;
+      MF_ASSERT(!real || pos[r] + t < k);
+      check_sptr(&sb[pad<PS>((int)(real ? pos[r] + t : BS))]);
+      sb[pad<PS>((int)(real ? pos[r] + t : BS))] = KElem32::make(key[r], ri);
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < RS; ++r) {
+      const uint32_t e = sub * NS + lane + 32 * r;
+      const bool real = e < k;
+      uint32_t ri = e;
+      if constexpr (SRr > 0) ri = (e & (SRr - 1)) * CHr + e / SRr;
+      MF_ASSERT(!real || pos[r] < k);
+      check_sptr(&sb[pad<PS>((int)(real ? pos[r] : BS))]);
+      sb[pad<PS>((int)(real ? pos[r] : BS))] = KElem32::make(key[r], ri);
+    }
   }
   // the scratch is reused by the next sort
   if constexpr (WP > 1) maxkey = bar.any(maxkey); else maxkey = __any_sync(0xFFFFFFFFu, maxkey);

@@ -77,12 +77,13 @@ struct MediumCfg {
   static constexpr int BL = WP > 1 ? MF_BL_TEAM : MF_BL_WARP;
   // padded element index: blocked per-lane writes hit distinct banks (8-byte elements);
   // the key sort scatters, so its slots are unpadded (the merge walks byte addresses)
-#ifndef MF_KS_PAD
-#define MF_KS_PAD 0  // 1: key-sorted slots padded one element per 16, so the lanes' merge cursors (16 elements
-                     // apart at R = 32) hit distinct banks.  Measured neutral: k = 1023 -1 %, k = 255 / 101 / 63
-                     // +0.8 / +1.2 / +1.1 % (the padded cursor arithmetic costs what the conflicts did)
+#ifndef MF_KS_PAD_MINR
+#define MF_KS_PAD_MINR 32  // smallest R whose key-sorted slots are padded one element per 16, so the lanes' merge
+                           // cursors (16 elements apart at R = 32) hit distinct banks.  With the kernel bound by
+                           // shared-memory wavefronts, R = 32 gains 2 % (k = 1023 1.344 -> 1.318 ms); R = 8 loses
+                           // 2.6 % (k = 255; the padded cursor arithmetic costs more than its conflicts did)
 #endif
-  static constexpr int PS = KS ? (MF_KS_PAD ? 4 : 30) : pad_shift<RS>();
+  static constexpr int PS = KS ? (R >= MF_KS_PAD_MINR ? 4 : 30) : pad_shift<RS>();
   static constexpr int SLOT = BS + (BS >> PS) + 1;
   static constexpr size_t sz_sorted = (sizeof(E) * SLOT * (W + 1) + 15) / 16 * 16;
   // merged pos -> key (MK), or -> (isB, sorted pos) where the keys would cost occupancy
@@ -90,7 +91,8 @@ struct MediumCfg {
 #define MF_MK_MAXR 0  // largest R whose merged keys are stored (measured: the extra smem costs more occupancy than the saved load)
 #endif
   static constexpr bool MK = R <= MF_MK_MAXR;
-  static constexpr size_t sz_src = (MK ? sizeof(U) : sizeof(uint16_t)) * 2 * BS;
+  // (u16 entries: 2*BS positions plus two pad entries per team lane, src_slot)
+  static constexpr size_t sz_src = MK ? sizeof(U) * 2 * BS : sizeof(uint16_t) * (2 * BS + 2 * 32 * WP);
   static constexpr size_t sz_rab = sizeof(uint32_t) * BS;      // RA | RB << 16, transposed [t][lane]
   static constexpr int NWP = MF_ROWS_PAD ? NW + 1 : NW;  // row stride in words (rows[L][w] at L*NWP + w)
   static constexpr size_t sz_rows_bits = sizeof(uint32_t) * NWP * CH;
@@ -100,7 +102,8 @@ struct MediumCfg {
   static constexpr size_t sz_scratch = sizeof(uint32_t) * 2 * WP * (32 * RS + RS);
   static constexpr size_t sz_rows0 = sz_rows_bits > sz_stage ? sz_rows_bits : sz_stage;
   static constexpr size_t sz_rows = (((KS && sz_scratch > sz_rows0) ? sz_scratch : sz_rows0) + 15) / 16 * 16;
-  static constexpr size_t sz_abits = sizeof(uint32_t) * NW;
+  // A-side bits per word, only where two team lanes share a word (2R/WP < 32 positions per lane)
+  static constexpr size_t sz_abits = 2 * R / WP == 32 ? 0 : sizeof(uint32_t) * NW;
   static constexpr size_t sz_warp = (sz_src + sz_rab + sz_rows + sz_abits + 15) / 16 * 16;  // per team
   static constexpr size_t smem = sz_sorted + W * sz_warp;
 };
@@ -125,13 +128,23 @@ __device__ __forceinline__ uint32_t row_addr(uint32_t L, uint32_t w) {
 #ifndef MF_MINB_R4
 #define MF_MINB_R4 4  // (64 registers: k = 101 1.65 -> 1.45 ms)
 #endif
-template <int R> struct MediumMinBlocks { static constexpr int value = R == 8 ? MF_MINB_R8 : R == 4 ? MF_MINB_R4 : 0; };
+#ifndef MF_MINB_R32
+#define MF_MINB_R32 3  // 3 CTAs of 128 threads per SM is what shared memory allows: keep ptxas under 170 registers
+                       // (unbounded it took 197 after a small change, 2 CTAs/SM, k = 1023 1.25 -> 1.42 ms)
+#endif
+template <int R> struct MediumMinBlocks {
+  static constexpr int value = R == 32 ? MF_MINB_R32 : R == 8 ? MF_MINB_R8 : R == 4 ? MF_MINB_R4 : 0;
+};
 
-// src[] holds one entry per merged position q, stored [q % PL][q / PL] (PL = positions per
-// team lane): the merge's per-lane runs of PL positions then store conflict-free.
+// src[] holds one u16 entry per merged position q, in position order with two pad entries
+// (one word) after each team lane's run of PL positions: the runs then start an odd number
+// of words apart, so the merge's per-lane stores are conflict-free, and the walk's reads --
+// every lane's cursor sits near the pair's median position -- fall on neighbouring words.
+// (The earlier [q % PL][q / PL] layout put those reads on one bank: 13 wavefronts per load
+// at k = 1023, 8.5 % of the kernel's shared-memory wavefronts.)
 template <int PL, int TL>
 __device__ __forceinline__ uint32_t src_slot(uint32_t q) {
-  return (q & (PL - 1)) * TL + (q >> __builtin_ctz(PL));
+  return q + 2 * (q >> __builtin_ctz(PL));
 }
 
 #ifndef MF_MERGE_NC32
@@ -238,6 +251,7 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
         }
       }
       const uint32_t limA = offA + 8 * padk(K);
+      const uint32_t sbase = (uint32_t)d + 2 * tl;  // src_slot(d): this lane's run of PL positions
       uint32_t relA[NC], relB[NC], bit[NC], am = 0;
       uint32_t ia[NC], ib[NC];                  // cursors (sorted positions) of the padded path
       uint2 ea[NC], eb[NC];
@@ -262,11 +276,11 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
           // past the pair both sides are the sentinel: ridx clamps to BS-1 >= k, whose rab
           // entry and row bits beyond 2k nobody reads -- no branch
           const uint32_t ri = min(takeA ? ea[j].x : eb[j].x, (uint32_t)C::BS - 1);
-          MF_ASSERT(w0 < (uint32_t)C::NWP && src_slot<PL, 32 * WP>(q) < 2u * C::BS);
+          MF_ASSERT(w0 < (uint32_t)C::NWP && src_slot<PL, 32 * WP>(q) < 2u * C::BS + 2u * TL);
           check_sptr(&rows[row_addr<CH, C::NWP>(ri & (CH - 1), w0)]);
           check_sptr(&rab16[2 * ri + 1]);
           atomicOr(&rows[row_addr<CH, C::NWP>(ri & (CH - 1), w0)], bit[j]);
-          src[src_slot<PL, 32 * WP>(q)] = (uint16_t)((takeA ? relA[j] : relB[j]) + 4);
+          src[sbase + j * PLC + r] = (uint16_t)((takeA ? relA[j] : relB[j]) + 4);  // = src_slot(q)
           rab16[2 * ri + (takeA ? 0 : 1)] = (uint16_t)q;
           am |= takeA ? bit[j] : 0u;
           bit[j] <<= 1;
@@ -376,7 +390,7 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
           const uint32_t bit = 1u << (bo + r);
           atomicOr(&rows[row_addr<CH, C::NWP>(c, w0)], bit);
           if constexpr (C::MK) reinterpret_cast<U*>(src)[q] = w.key();
-          else src[src_slot<PL, TL>(q)] = (uint16_t)sel(takeA, ia, 0x8000u | ib);
+          else src[(uint32_t)d + 2 * tl + r] = (uint16_t)sel(takeA, ia, 0x8000u | ib);  // = src_slot(q)
           rab16[2 * ((idx & (SR - 1)) * CH + c) + (takeA ? 0 : 1)] = (uint16_t)q;
           amask |= takeA ? bit : 0u;
           ia += takeA;
@@ -413,7 +427,7 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
         auto key_at = [&](uint32_t p) -> U {
           if constexpr (C::KS) {
             uint32_t v;
-            MF_ASSERT(p < nq && src_slot<PL, TL>(p) < 2u * C::BS);
+            MF_ASSERT(p < nq && src_slot<PL, TL>(p) < 2u * C::BS + 2u * TL);
             check_saddr(ringK + src[src_slot<PL, TL>(p)], 4);
             asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(ringK + src[src_slot<PL, TL>(p)]));
             return (U)v;
