@@ -39,10 +39,13 @@ namespace mf {
 #endif
 
 #ifndef MF_WALK_WT
-#define MF_WALK_WT 1  // the walk writes every Delete/Undelete through to the rows (two atomics per step).
-                      // 0 (rows kept at their chunk-start value, a word rebuilt by replaying the chunk's
-                      // steps when the cursor enters it) measured slower: k = 1023 1.41 -> 1.84 ms, k = 255
-                      // 0.98 -> 1.09 ms -- the cursor changes words far more often than once a chunk
+#define MF_WALK_WT 1  // how the walk keeps the rows current.  1: every Delete/Undelete is written through (two
+                      // atomics per step on random words of the lane's row).  2: only the three words around
+                      // the chunk's first cursor word are written through; a word outside that window keeps its
+                      // chunk-start value and is rebuilt by replaying the chunk's steps when the cursor enters
+                      // it -- fewer shared-memory wavefronts, but measured slower (k = 1023 1.229 -> 1.306 ms,
+                      // k = 255 0.927 -> 0.964 ms: the window tests cost more than the atomics).  0: no
+                      // write-through at all (k = 1023 1.41 -> 1.84 ms)
 #endif
 #ifndef MF_ROWS_PAD
 #define MF_ROWS_PAD 1
@@ -470,6 +473,8 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
             cnt += sg;
           }
           uint32_t p = cw * 32 + __fns(cb, 0, (int)(h - cnt) + 1);
+          const uint32_t cw0 = cw;  // the written-through window is [cw0 - 1, cw0 + 1] (MF_WALK_WT = 2)
+          (void)cw0;
           out[0] = key_at(p);
 #pragma unroll
           for (int t = 1; t < SR; ++t) {
@@ -482,9 +487,12 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
               // also written through to the row (fire-and-forget atomics), else the row keeps its
               // chunk-start value and a word the cursor moves into is rebuilt from it and the
               // chunk's earlier steps (rare)
-#if MF_WALK_WT
+#if MF_WALK_WT == 1
               atomicAnd(&rows[row_addr<CH, C::NWP>(tl, a >> 5)], ~ba);
               atomicOr(&rows[row_addr<CH, C::NWP>(tl, b >> 5)], bb);
+#elif MF_WALK_WT == 2
+              if ((a >> 5) + 1 - cw0 <= 2u) atomicAnd(&rows[row_addr<CH, C::NWP>(tl, a >> 5)], ~ba);
+              if ((b >> 5) + 1 - cw0 <= 2u) atomicOr(&rows[row_addr<CH, C::NWP>(tl, b >> 5)], bb);
 #endif
               cb = sel((a >> 5) == cw, cb & ~ba, cb);
               cb = sel((b >> 5) == cw, cb | bb, cb);
@@ -501,9 +509,9 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
                   cw += dir;
                   MF_ASSERT(cw < nw);
                   cb = rows[row_addr<CH, C::NWP>(tl, cw)];
-#if !MF_WALK_WT
+#if MF_WALK_WT != 1
 #pragma unroll 1
-                  for (int tt = 1; tt <= t; ++tt) {  // replay this chunk's steps so far on word cw
+                  for (int tt = 1; tt <= (MF_WALK_WT == 2 && cw + 1 - cw0 <= 2u ? 0 : t); ++tt) {  // replay this chunk's steps so far on word cw
                     const uint32_t ab2 = rab[(tt - 1) * CH + tl];
                     const uint32_t a2 = ab2 & 0xFFFF, b2 = ab2 >> 16;
                     cb = sel((a2 >> 5) == cw, cb & ~(1u << (a2 & 31)), cb);
