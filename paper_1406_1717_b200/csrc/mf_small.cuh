@@ -70,6 +70,10 @@ template <int DT, int K> struct SmallShape {
   static_assert(T >= K, "small-kernel CTA must have at least K threads");
 };
 
+#ifndef MF_SMALL_FAST_MAXK
+#define MF_SMALL_FAST_MAXK 31  // largest k with the sentinel-row walk variant (k = 5..31: 10-16 % faster; past 31 the
+                               // second copy of the unrolled walk and the extra key row cost more than they save)
+#endif
 template <int DT, int K, int T>
 struct SmallCfg {
   using Tr = Traits<DT>;
@@ -81,8 +85,9 @@ struct SmallCfg {
   static constexpr int SC = TU + 32;                    // column stride: >= NB, a multiple of 32
   // one input buffer (bytes): NB*K elements plus up to 16 bytes of alignment shift
   static constexpr int IO = (NB * K * (int)sizeof(U) + 15) / 16 * 16 + 16;
-  static constexpr size_t off_key = 0;                                          // U[K*SC]
-  static constexpr size_t off_rank = off_key + sizeof(U) * K * SC;              // u8[K*SC]
+  static constexpr bool FAST = K <= MF_SMALL_FAST_MAXK;                         // sentinel row + fast walk variant
+  static constexpr size_t off_key = 0;                                          // U[K*SC] (+ the sentinel row K)
+  static constexpr size_t off_rank = off_key + sizeof(U) * (K + (FAST ? 1 : 0)) * SC;  // u8[K*SC]
   static constexpr size_t off_io = (off_rank + K * SC + 15) / 16 * 16;          // 2 x IO bytes
   static constexpr size_t smem = off_io + 2 * (size_t)IO;
 };
@@ -175,6 +180,9 @@ __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_
   uint64_t row = t_begin / tiles_per_row, tr = t_begin % tiles_per_row;
   auto xrow = [&](uint64_t r) { return reinterpret_cast<const TV*>(g.x) + r * g.ld_x; };
   if (t_begin < t_end) stage_tile<TV, NB * K, T>(io(0), xrow(row), g.n, tr * TU * K);
+  // sorted position K of every column: the list's sentinel node k (block.hpp:21-24), an all-ones key
+  if constexpr (C::FAST)
+    for (int c = t; c < SC; c += T) skey[K * SC + c] = UMax<U>::v;
   int cur = 0;
   bool carried = false;                   // column 0 already holds this tile's first block
   for (uint64_t tt = t_begin; tt < t_end; ++tt, cur ^= 1) {
@@ -212,9 +220,13 @@ __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_
     const uint64_t obase = u0 * K;
     const int omis = misalign(y + obase);
     U* ost = reinterpret_cast<U*>(io(cur) + omis);  // natural layout, odd K: conflict-free
-#pragma unroll 1
-    for (int j = 0; j < UPT; ++j) {
-      const uint32_t c = t + T * j;
+    // The walk of one unit.  EXACT = false: neither block holds a real all-ones key (the usual
+    // case), so the sentinel row orders Peek(A) against Peek(B) by a plain key compare -- an
+    // exhausted list peeks the all-ones key, which no live element ties with -- and the
+    // emitted value is the smaller peek.  EXACT = true keeps the explicit sentinel tests
+    // (ties go to A; the sentinel is never smaller, filter.hpp:90-95).
+    auto walk_unit = [&](auto exact_tag, uint32_t c) {
+      constexpr bool EXACT = decltype(exact_tag)::value;
       const U* kA = skey + c;
       const U* kB = skey + c + 1;
       const uint8_t* rA = srank + c;
@@ -244,14 +256,29 @@ __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_
         maskB |= (M)1 << rb;
         mB = sel(rb < mB, live_prev(maskB, mB, KK), mB);
         // Balance: filter.hpp:90-95 (ties go to A; the sentinel is never smaller)
-        keyA = sel(mA == KK, UMax<U>::v, kA[min(mA, KK - 1) * SC]);
-        keyB = sel(mB == KK, UMax<U>::v, kB[min(mB, KK - 1) * SC]);
         const bool need = (int)(sA + sB) < H;
-        const bool bLess = (mB != KK) && (mA == KK || keyB < keyA);
+        if constexpr (EXACT) {
+          keyA = sel(mA == KK, UMax<U>::v, kA[min(mA, KK - 1) * SC]);
+          keyB = sel(mB == KK, UMax<U>::v, kB[min(mB, KK - 1) * SC]);
+        } else {
+          keyA = kA[mA * SC];
+          keyB = kB[mB * SC];
+        }
+        const bool bLess = EXACT ? (mB != KK) && (mA == KK || keyB < keyA) : keyB < keyA;
         const bool advA = need && !bLess, advB = need && bLess;
 #if MF_SMALL_ONE_SUCC
-        // at most one side advances: one successor search on the selected list
-        const uint32_t nxt = live_succ(bLess ? maskB : maskA, bLess ? mB : mA, KK);
+        // at most one side advances: one successor search on the selected list.  Without real
+        // all-ones keys a list that must advance is never at its sentinel (keyB < keyA rules it out
+        // for B; for A both peeks would be sentinels, i.e. every live element is already small and
+        // `need` is false), so the successor is the next live position above the cursor; the two
+        // one-position shifts keep the unused result of a cursor at K defined.
+        uint32_t nxt;
+        if constexpr (EXACT) {
+          nxt = live_succ(bLess ? maskB : maskA, bLess ? mB : mA, KK);
+        } else {
+          const uint32_t ms = bLess ? mB : mA;
+          nxt = ms + ffs_m((M)((M)((bLess ? maskB : maskA) >> 1) >> ms));
+        }
         mA = sel(advA, nxt, mA);
         mB = sel(advB, nxt, mB);
 #else
@@ -260,13 +287,33 @@ __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_
 #endif
         sA += advA;
         sB += advB;
-        const U* kp = advA ? kA + min(mA, KK - 1) * SC : kB + min(mB, KK - 1) * SC;
-        const U kn = *kp;
-        keyA = sel(mA == KK, UMax<U>::v, sel(advA, kn, keyA));
-        keyB = sel(mB == KK, UMax<U>::v, sel(advB, kn, keyB));
-        // Emit min{Peek(A), Peek(B)}: filter.hpp:97-100
-        const bool bLess2 = (mB != KK) && (mA == KK || keyB < keyA);
-        ost[c * K + i] = sel(bLess2, keyB, keyA);
+        if constexpr (EXACT) {
+          const U* kp = advA ? kA + min(mA, KK - 1) * SC : kB + min(mB, KK - 1) * SC;
+          const U kn = *kp;
+          keyA = sel(mA == KK, UMax<U>::v, sel(advA, kn, keyA));
+          keyB = sel(mB == KK, UMax<U>::v, sel(advB, kn, keyB));
+          // Emit min{Peek(A), Peek(B)}: filter.hpp:97-100
+          const bool bLess2 = (mB != KK) && (mA == KK || keyB < keyA);
+          ost[c * K + i] = sel(bLess2, keyB, keyA);
+        } else {
+          const U* kp = advA ? kA + mA * SC : kB + mB * SC;
+          const U kn = *kp;
+          keyA = sel(advA, kn, keyA);
+          keyB = sel(advB, kn, keyB);
+          ost[c * K + i] = min(keyA, keyB);   // Emit min{Peek(A), Peek(B)}: filter.hpp:97-100
+        }
+      }
+    };
+#pragma unroll 1
+    for (int j = 0; j < UPT; ++j) {
+      const uint32_t c = t + T * j;
+      // a block's largest key sits at sorted position K-1
+      if constexpr (C::FAST) {
+        const bool exact = skey[(K - 1) * SC + c] == UMax<U>::v || skey[(K - 1) * SC + c + 1] == UMax<U>::v;
+        if (exact) walk_unit(std::true_type{}, c);
+        else walk_unit(std::false_type{}, c);
+      } else {
+        walk_unit(std::true_type{}, c);
       }
     }
     __syncthreads();
