@@ -59,8 +59,11 @@ struct MediumCfg {
 #ifndef MF_KEYSORT
 #define MF_KEYSORT 1  // 32-bit keys: key-only network + rank recovery (team_sort_keys)
 #endif
-  // (R = 16: measured 2 % slower with it, the payload network is kept there)
-  static constexpr bool KS = MF_KEYSORT && sizeof(U) == 4 && R != 16;
+#ifndef MF_KS_R16
+#define MF_KS_R16 1  // R = 16 (k = 257..511) on the key-only sort too: with 4 teams per CTA and 4 CTAs per SM,
+                     // k = 257 / 385 / 511 2.30 / 1.58 / 1.20 -> 1.90 / 1.32 / 1.04 ms (round 1 had it 2 % slower)
+#endif
+  static constexpr bool KS = MF_KEYSORT && sizeof(U) == 4 && (R != 16 || MF_KS_R16);
   using E = std::conditional_t<(KS || R <= MF_MEDIUM_KEYORD_MAXR), typename KeyOrd<U>::E, Elem<U>>;
   static constexpr int BS = 32 * R;        // block slot capacity (>= k)
   static constexpr int NW = 2 * R;         // words per merged row (2k bits <= 64R)
@@ -131,12 +134,15 @@ __device__ __forceinline__ uint32_t row_addr(uint32_t L, uint32_t w) {
 #ifndef MF_MINB_R4
 #define MF_MINB_R4 4  // (64 registers: k = 101 1.65 -> 1.45 ms)
 #endif
+#ifndef MF_MINB_R16
+#define MF_MINB_R16 4  // 128 registers: 4 CTAs of 4 teams per SM (168 registers and 3 CTAs: k = 511 1.08 ms; 4: 1.04 ms)
+#endif
 #ifndef MF_MINB_R32
 #define MF_MINB_R32 3  // 3 CTAs of 128 threads per SM is what shared memory allows: keep ptxas under 170 registers
                        // (unbounded it took 197 after a small change, 2 CTAs/SM, k = 1023 1.25 -> 1.42 ms)
 #endif
 template <int R> struct MediumMinBlocks {
-  static constexpr int value = R == 32 ? MF_MINB_R32 : R == 8 ? MF_MINB_R8 : R == 4 ? MF_MINB_R4 : 0;
+  static constexpr int value = R == 32 ? MF_MINB_R32 : R == 16 ? MF_MINB_R16 : R == 8 ? MF_MINB_R8 : R == 4 ? MF_MINB_R4 : 0;
 };
 
 // src[] holds one u16 entry per merged position q, in position order with two pad entries

@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_
       M maskA = SENT | (SENT - 1u);  // construct: all live, s = h, m = pi[h] (block.hpp:47-49)
       uint32_t mA = H, sA = H;
       M maskB = SENT;
-      uint32_t mB = K, sB = 0;  // unwind: empty, m = k, s = 0 (block.hpp:62-63)
+      uint32_t mB = K;          // unwind: empty, m = k, s = 0 (block.hpp:62-63)
       U keyA = kA[H * SC], keyB = UMax<U>::v;
       ost[c * K] = keyA;                      // Peek of the constructed block (filter.hpp:81-82)
 #pragma unroll
@@ -249,14 +249,19 @@ __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_
         maskA &= ~((M)1 << ra);
         const bool belowA = ra < mA;
         const uint32_t m1 = sel(ra == mA, live_next(maskA, ra), mA);
-        const uint32_t pv = live_prev(maskA, m1, KK);
+        // (prev of the moved cursor = highest live below the old one: ra itself is deleted and
+        // nothing live lies between it and its successor -- one step off the dependency chain)
+        const uint32_t pv = live_prev(maskA, mA, KK);
         mA = sel(!belowA && sA > 0, pv, m1);
-        sA -= (belowA || sA > 0) ? 1u : 0u;
+        // s_A + s_B = h holds before every step (Balance restores it with its single advance), so
+        // Balance must advance exactly when Delete took a small element away; s_B = h - s_A is
+        // not carried
+        const bool need = belowA || sA > 0;
+        sA -= need ? 1u : 0u;
         // Undelete(B, i-1): block.hpp:89-98
         maskB |= (M)1 << rb;
         mB = sel(rb < mB, live_prev(maskB, mB, KK), mB);
         // Balance: filter.hpp:90-95 (ties go to A; the sentinel is never smaller)
-        const bool need = (int)(sA + sB) < H;
         if constexpr (EXACT) {
           keyA = sel(mA == KK, UMax<U>::v, kA[min(mA, KK - 1) * SC]);
           keyB = sel(mB == KK, UMax<U>::v, kB[min(mB, KK - 1) * SC]);
@@ -286,7 +291,6 @@ __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_
         mB = sel(advB, live_succ(maskB, mB, KK), mB);
 #endif
         sA += advA;
-        sB += advB;
         if constexpr (EXACT) {
           const U* kp = advA ? kA + min(mA, KK - 1) * SC : kB + min(mB, KK - 1) * SC;
           const U kn = *kp;
