@@ -454,7 +454,13 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_med
         U out[SR];
         if (i0 < imax) {
           // select the (h+1)-th live position of row_L, G independent words at a time
-          constexpr int G = R >= 16 ? 4 : 1;
+#ifndef MF_SEL_G_SMALL
+#define MF_SEL_G_SMALL 1
+#endif
+#ifndef MF_SEL_G_LARGE
+#define MF_SEL_G_LARGE 4
+#endif
+          constexpr int G = R >= 16 ? MF_SEL_G_LARGE : MF_SEL_G_SMALL;
           uint32_t cnt = 0, cw = 0, cb = 0;
           for (;; cw += G) {
             uint32_t wv[G], pc[G], sg = 0;

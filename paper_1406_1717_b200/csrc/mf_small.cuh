@@ -131,12 +131,48 @@ __device__ __forceinline__ int misalign(const TV* p) {
   return (int)((reinterpret_cast<uintptr_t>(p) & 15) / sizeof(TV));
 }
 
-// Stage NE elements (raw input bits from x + base) into `buf`.  Whole 16-byte chunks
-// inside [0, n) go through cp.async; the ragged head/tail and the padding past n (the
-// reference's +INF sentinels, filter.hpp:28-36) are written directly.  The padding value
-// 0x7FF..F maps to the all-ones ukey for every dtype.
+// TMA bulk copy (cp.async.bulk, the 1-D form of the tensor memory accelerator): one thread
+// issues one asynchronous global -> shared copy for the whole aligned body of a tile and the
+// copy engine signals an mbarrier with the bytes it wrote, so no thread spends issue slots or
+// address arithmetic on the staging loads.
+#ifndef MF_SMALL_TMA
+#define MF_SMALL_TMA 1  // 0: per-thread 16-byte cp.async chunks (the round-1 loader)
+#endif
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+// orders this CTA's earlier generic-proxy accesses of shared memory before later async-proxy ones
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(d), "l"(gmem_src), "r"(bytes), "r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t ok;
+  do {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+  } while (!ok);
+}
+
+// Stage NE elements (raw input bits from x + base) into `buf`.  The whole 16-byte chunks
+// inside [0, n) move as one TMA bulk copy that completes on `bar` (every call arms one phase
+// of it, with zero bytes when the tile has no aligned body); the ragged head/tail and the
+// padding past n (the reference's +INF sentinels, filter.hpp:28-36) are written directly.
+// The padding value 0x7FF..F maps to the all-ones ukey for every dtype.  The caller has
+// synchronised the CTA after its last generic access of `buf`.
 template <typename TV, int NE, int T>
-__device__ __forceinline__ void stage_tile(TV* buf, const TV* x, uint64_t n, uint64_t base) {
+__device__ __forceinline__ void stage_tile(TV* buf, const TV* x, uint64_t n, uint64_t base, uint64_t* bar) {
   constexpr int EPC = 16 / (int)sizeof(TV);  // elements per 16-byte chunk
   const TV pad = (TV)(~(std::make_unsigned_t<TV>)0 >> 1);
   const int mis = misalign(x + base);
@@ -146,10 +182,21 @@ __device__ __forceinline__ void stage_tile(TV* buf, const TV* x, uint64_t n, uin
   const int h0 = min((EPC - mis) % EPC, real);   // unaligned head elements
   const int nchunks = (real - h0) / EPC;
   const int tail0 = h0 + nchunks * EPC;
+#if MF_SMALL_TMA
+  if (threadIdx.x == 0) {
+    fence_proxy_async();
+    mbar_expect_tx(bar, (uint32_t)nchunks * 16u);
+    if (nchunks > 0) tma_load_1d(dst + h0, src + h0, (uint32_t)nchunks * 16u, bar);
+  }
+#else
+  (void)bar;
   for (int c = threadIdx.x; c < nchunks; c += T) cp_async16(dst + h0 + c * EPC, src + h0 + c * EPC);
+#endif
   if ((int)threadIdx.x < h0) dst[threadIdx.x] = src[threadIdx.x];
   for (int e = tail0 + threadIdx.x; e < NE; e += T) dst[e] = e < real ? src[e] : pad;
+#if !MF_SMALL_TMA
   cp_async_commit();
+#endif
 }
 
 #ifndef MF_SMALL_ONE_SUCC
@@ -179,7 +226,16 @@ __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_
   // (row, tile-in-row) of the current tile, advanced incrementally (no 64-bit division)
   uint64_t row = t_begin / tiles_per_row, tr = t_begin % tiles_per_row;
   auto xrow = [&](uint64_t r) { return reinterpret_cast<const TV*>(g.x) + r * g.ld_x; };
-  if (t_begin < t_end) stage_tile<TV, NB * K, T>(io(0), xrow(row), g.n, tr * TU * K);
+  // one mbarrier per input buffer; buffer b's phase flips every time it is refilled
+  __shared__ __align__(8) uint64_t tile_bar[2];
+  uint32_t bar_phase = 0;                 // bit b: parity to wait for on tile_bar[b]
+  if (t == 0) {
+    mbar_init(&tile_bar[0], 1);
+    mbar_init(&tile_bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (t_begin < t_end) stage_tile<TV, NB * K, T>(io(0), xrow(row), g.n, tr * TU * K, &tile_bar[0]);
   // sorted position K of every column: the list's sentinel node k (block.hpp:21-24), an all-ones key
   if constexpr (C::FAST)
     for (int c = t; c < SC; c += T) skey[K * SC + c] = UMax<U>::v;
@@ -191,9 +247,14 @@ __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_
     const uint64_t u0 = tr * TU;
     uint64_t nrow = row, ntr = tr + 1;
     if (ntr == tiles_per_row) { ntr = 0; ++nrow; }
+#if MF_SMALL_TMA
+    mbar_wait(&tile_bar[cur], (bar_phase >> cur) & 1u);
+    bar_phase ^= 1u << cur;
+#else
     cp_async_wait_all();
+#endif
     __syncthreads();                      // tile tt landed; previous tile fully consumed
-    if (tt + 1 < t_end) stage_tile<TV, NB * K, T>(io(cur ^ 1), xrow(nrow), g.n, ntr * TU * K);  // prefetch
+    if (tt + 1 < t_end) stage_tile<TV, NB * K, T>(io(cur ^ 1), xrow(nrow), g.n, ntr * TU * K, &tile_bar[cur ^ 1]);  // prefetch
     TV* in = io(cur) + misalign(x + u0 * K);
 
     // ---- phase 1: sort column c (= block u0+c) in registers ----
