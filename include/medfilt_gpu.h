@@ -41,7 +41,7 @@ typedef enum {
 
 typedef enum { MF_I32 = 0, MF_I64 = 1, MF_F32 = 2, MF_F64 = 3 } mf_dtype;
 
-/* Kernel classes chosen by k: fused small (k <= 31; k <= 53 for 32-bit
+/* Kernel classes chosen by k: fused small (k <= 31; k <= 63 for 32-bit
  * keys; k = 3 is a direct selection kernel inside this class), fused medium (k <= 1023),
  * multi-kernel large. */
 typedef enum { MF_CLASS_AUTO = -1, MF_CLASS_SMALL = 0, MF_CLASS_MEDIUM = 1, MF_CLASS_LARGE = 2 } mf_class;

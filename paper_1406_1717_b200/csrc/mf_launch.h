@@ -36,10 +36,10 @@ void phase_end(cudaStream_t s);                  // closes the last phase, stops
 // Largest k each fused class handles (per key width).
 constexpr uint32_t kSmallMaxK = 31;        // 64-bit keys
 #ifndef MF_SMALL_MAXK32
-#define MF_SMALL_MAXK32 53
+#define MF_SMALL_MAXK32 63
 #endif
 constexpr uint32_t kSmallMaxK32 = MF_SMALL_MAXK32;      // 32-bit keys (64-bit live masks past 31; the medium
-                                           // kernel measured faster from k = 55 on)
+                                           // kernel takes over at k = 65)
 inline uint32_t small_max_k(int dt) { return (dt == DT_I32 || dt == DT_F32) ? kSmallMaxK32 : kSmallMaxK; }
 constexpr uint32_t kMediumMaxK = 1023;
 // Largest k of the large-k pipeline: it packs 2k merged positions (padded to a multiple of
@@ -49,7 +49,7 @@ constexpr uint64_t kLargeMaxK = (uint64_t(1) << 31) - 65;
 
 // Fused small-k kernel (k odd, k <= small_max_k(dt)).
 cudaError_t launch_small(int dt, const Geom& g, cudaStream_t s, uint64_t* launches);
-// ... its 33 <= k <= 53 instantiations (32-bit keys; mf_small63.cu)
+// ... its 33 <= k <= 63 instantiations (32-bit keys; mf_small63.cu)
 cudaError_t launch_small_k63(int dt, const Geom& g, cudaStream_t s);
 // Fused medium-k kernel (k <= 1023).
 cudaError_t launch_medium(int dt, const Geom& g, cudaStream_t s, uint64_t* launches);

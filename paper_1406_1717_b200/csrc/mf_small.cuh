@@ -1,4 +1,4 @@
-// mf_small.cuh -- fused median filter for small windows (k <= 31, and k <= 53 for 32-bit
+// mf_small.cuh -- fused median filter for small windows (k <= 31, and k <= 63 for 32-bit
 // keys): one thread per block pair, both phases in one pass over HBM.
 //
 // Reference path replaced: median_filter<T> (filter.hpp:149-155) for k <= 31:
@@ -36,6 +36,9 @@ template <int DT, int K> struct SmallShape {
 #ifndef MF_SMALL_T_K31
 #define MF_SMALL_T_K31 512  // (experiments: tile shape of k = 24..31, 32-bit keys)
 #endif
+#ifndef MF_SMALL_T_K23
+#define MF_SMALL_T_K23 256  // k = 9..23
+#endif
 #ifndef MF_SMALL_UPT_K31
 #define MF_SMALL_UPT_K31 1
 #endif
@@ -45,25 +48,33 @@ template <int DT, int K> struct SmallShape {
 #ifndef MF_SMALL_UPT_K3
 #define MF_SMALL_UPT_K3 4
 #endif
+  // 33 <= k <= 53, re-measured after the column sort became a single inlined call site (no
+  // local-memory element array any more): T = 64 / 96 / 128 / 256 gave, in ms on the c2 signal,
+  //   k = 37: 1.10 / 1.07 / 1.02 / 0.70    k = 41: 1.31 / 1.27 / 0.94 / 0.73    k = 43: 1.28 / 1.29 / 0.91 / 0.83
+  //   k = 45: 1.30 / 1.26 / 0.97 / 1.02    k = 47: 1.12 / 1.21 / 1.10 / 1.12    k = 49: 1.15 / 1.20 / 1.15 / 1.15
+  //   k = 51: 1.14 / 1.08 / 1.14 / 1.14    k = 53: 1.14 / 1.11 / 1.15 / 1.16
 #ifndef MF_SMALL_T_K35
-#define MF_SMALL_T_K35 256  // k = 33, 35 (32-bit keys, 64-bit masks): measured 0.72 ms at k = 33 (128: 0.97)
+#define MF_SMALL_T_K35 256  // k = 33, 35: 0.64 / 0.71 ms (128: 1.02 / 1.03)
 #endif
-#ifndef MF_SMALL_T_K41
-#define MF_SMALL_T_K41 128  // k = 37..41: measured 0.96 / 0.98 ms at k = 37 / 41 (256: 1.05 / 1.45)
-#endif
-#ifndef MF_SMALL_T_K45
-#define MF_SMALL_T_K45 64   // k = 43, 45: 1.20 ms at k = 45 (128: 1.43; smaller tiles fit more CTAs)
-#endif
-#ifndef MF_SMALL_T_K53
-#define MF_SMALL_T_K53 96   // k = 49..53: 1.30 / 1.28 / 1.30 ms (64: 1.45; the medium kernel: 1.64 / 1.57 / 1.51)
+#ifndef MF_SMALL_T_K43
+#define MF_SMALL_T_K43 256  // k = 37..43
 #endif
 #ifndef MF_SMALL_T_K47
-#define MF_SMALL_T_K47 96   // k = 47: 1.30 ms (128: 1.44, 64: 1.44)
+#define MF_SMALL_T_K47 128  // k = 45, 47
+#endif
+#ifndef MF_SMALL_T_K49
+#define MF_SMALL_T_K49 128  // k = 49
+#endif
+#ifndef MF_SMALL_T_K53
+#define MF_SMALL_T_K53 96   // k = 51, 53
+#endif
+#ifndef MF_SMALL_T_K63
+#define MF_SMALL_T_K63 128  // k = 55..63: 1.17 ms each (96: 1.48 / 1.51 / 1.49; 256: 1.18; the medium kernel: 1.38 / 1.30 / 1.22)
 #endif
   static constexpr int T = wide ? 128
-                                : (K <= 5 ? MF_SMALL_T_K3 : K <= 7 ? 512 : K <= 23 ? 256 : K <= 31 ? MF_SMALL_T_K31
-                                   : K <= 35 ? MF_SMALL_T_K35 : K <= 41 ? MF_SMALL_T_K41
-                                   : K <= 45 ? MF_SMALL_T_K45 : K <= 47 ? MF_SMALL_T_K47 : MF_SMALL_T_K53);
+                                : (K <= 5 ? MF_SMALL_T_K3 : K <= 7 ? 512 : K <= 23 ? MF_SMALL_T_K23 : K <= 31 ? MF_SMALL_T_K31
+                                   : K <= 35 ? MF_SMALL_T_K35 : K <= 43 ? MF_SMALL_T_K43
+                                   : K <= 47 ? MF_SMALL_T_K47 : K <= 49 ? MF_SMALL_T_K49 : K <= 53 ? MF_SMALL_T_K53 : MF_SMALL_T_K63);
   static constexpr int UPT = wide ? (K <= 7 ? 4 : K <= 15 ? 2 : 1)
                                   : (K <= 5 ? MF_SMALL_UPT_K3 : K <= 11 ? 2 : K <= 23 ? 1 : MF_SMALL_UPT_K31);
   // the cross-tile carry of the last block is spread over the first K threads (t < K)
@@ -270,9 +281,11 @@ __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_
         srank[v[p].idx() * SC + c] = (uint8_t)p;
       }
     };
-#pragma unroll
-    for (int j = 0; j < UPT; ++j) sort_column(t + T * j + 1);
-    if (!carried && t == 0) sort_column(0);
+    // one call site, not unrolled: a single copy of the network, always inlined (with two call
+    // sites nvcc outlined the column sort at k = 29, 31 and the element array went through
+    // local memory).  Thread 0 also sorts column 0 when the previous tile did not carry it.
+#pragma unroll 1
+    for (int j = (!carried && t == 0) ? -1 : 0; j < UPT; ++j) sort_column(j < 0 ? 0u : t + T * j + 1);
     __syncthreads();                      // columns ready; `in` is free for output staging
 
     // ---- phase 2: Figure-7 postprocess for unit (A = column c, B = column c+1) ----

@@ -49,6 +49,17 @@ template <int K> struct OEM { static constexpr NetList net = make_oem(K); };
 // ---- element types --------------------------------------------------------------------
 template <typename U> struct Elem;
 
+// High word of a packed (key << 32 | index) element as a 32-bit register.  Written as a
+// register-pair split because nvcc otherwise compares `(uint32_t)(v >> 32)` values as 64-bit
+// numbers with a zero high word: an ISETP plus a useless ISETP.EX on (RZ, RZ) per exchange
+// (378 of them in the k = 31 network).
+__device__ __forceinline__ uint32_t hi32(uint64_t v) {
+  uint32_t lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
+  (void)lo;
+  return hi;
+}
+
 template <> struct Elem<uint32_t> {
   static constexpr bool kFull = true;  // totally ordered by (key, index)
   uint64_t v;  // key << 32 | index
@@ -59,7 +70,7 @@ template <> struct Elem<uint32_t> {
   __device__ __forceinline__ static Elem sentinel() { Elem e; e.v = ~0ull; return e; }
   // merge order of two sorted blocks (A before B on ties): the sort order itself
   __device__ __forceinline__ static bool merge_le(const Elem& a, const Elem& b) { return a.v <= b.v; }
-  __device__ __forceinline__ uint32_t key() const { return (uint32_t)(v >> 32); }
+  __device__ __forceinline__ uint32_t key() const { return hi32(v); }
   __device__ __forceinline__ uint32_t idx() const { return (uint32_t)v; }
   __device__ __forceinline__ static bool less(const Elem& x, const Elem& y) { return x.v < y.v; }
   __device__ __forceinline__ static bool less_full(const Elem& x, const Elem& y) { return x.v < y.v; }
@@ -121,7 +132,7 @@ struct KElem32 {
   __device__ __forceinline__ static bool merge_le(const KElem32& a, const KElem32& b) {
     return (a.v & 0xFFFFFFFF80000000ull) <= (b.v & 0xFFFFFFFF80000000ull);
   }
-  __device__ __forceinline__ uint32_t key() const { return (uint32_t)(v >> 32); }
+  __device__ __forceinline__ uint32_t key() const { return hi32(v); }
   __device__ __forceinline__ uint32_t idx() const { return (uint32_t)v; }
   __device__ __forceinline__ static bool less(const KElem32& x, const KElem32& y) { return x.key() < y.key(); }
   __device__ __forceinline__ static bool less_full(const KElem32& x, const KElem32& y) { return x.v < y.v; }

@@ -73,8 +73,8 @@ def test_host_entry_validates_before_device():
 def test_kernel_classes():
     assert mf.kernel_class(np.float32, 3) == N.MF_CLASS_SMALL
     assert mf.kernel_class(np.float32, 31) == N.MF_CLASS_SMALL
-    assert mf.kernel_class(np.int32, 53) == N.MF_CLASS_SMALL      # 64-bit live masks
-    assert mf.kernel_class(np.int32, 55) == N.MF_CLASS_MEDIUM
+    assert mf.kernel_class(np.int32, 63) == N.MF_CLASS_SMALL      # 64-bit live masks
+    assert mf.kernel_class(np.int32, 65) == N.MF_CLASS_MEDIUM
     assert mf.kernel_class(np.float64, 33) == N.MF_CLASS_MEDIUM   # 64-bit keys stop at 31
     assert mf.kernel_class(np.float32, 65) == N.MF_CLASS_MEDIUM
     assert mf.kernel_class(np.int32, 1023) == N.MF_CLASS_MEDIUM
