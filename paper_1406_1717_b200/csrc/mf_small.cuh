@@ -330,8 +330,8 @@ __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_
         // s_A + s_B = h holds before every step (Balance restores it with its single advance), so
         // Balance must advance exactly when Delete took a small element away; s_B = h - s_A is
         // not carried
+        // (s_A then changes by advA - need = -advB: need && !advB is need && advA)
         const bool need = belowA || sA > 0;
-        sA -= need ? 1u : 0u;
         // Undelete(B, i-1): block.hpp:89-98
         maskB |= (M)1 << rb;
         mB = sel(rb < mB, live_prev(maskB, mB, KK), mB);
@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(T) mf_small_kernel(Geom g, uint64_t tiles_per_
         mA = sel(advA, live_succ(maskA, mA, KK), mA);
         mB = sel(advB, live_succ(maskB, mB, KK), mB);
 #endif
-        sA += advA;
+        sA -= advB ? 1u : 0u;
         if constexpr (EXACT) {
           const U* kp = advA ? kA + min(mA, KK - 1) * SC : kB + min(mB, KK - 1) * SC;
           const U kn = *kp;
