@@ -141,8 +141,14 @@ __device__ __forceinline__ uint32_t row_addr(uint32_t L, uint32_t w) {
 #define MF_MINB_R32 3  // 3 CTAs of 128 threads per SM is what shared memory allows: keep ptxas under 170 registers
                        // (unbounded it took 197 after a small change, 2 CTAs/SM, k = 1023 1.25 -> 1.42 ms)
 #endif
-template <int R> struct MediumMinBlocks {
-  static constexpr int value = R == 32 ? MF_MINB_R32 : R == 16 ? MF_MINB_R16 : R == 8 ? MF_MINB_R8 : R == 4 ? MF_MINB_R4 : 0;
+#ifndef MF_MINB_R4_WIDE
+#define MF_MINB_R4_WIDE 6  // R = 4, 64-bit keys (config 1): 6 CTAs of 4 teams per SM (80 registers); 4 CTAs (103
+                           // registers): c1 0.0542 -> 0.0474 ms
+#endif
+template <int DT, int R> struct MediumMinBlocks {
+  static constexpr bool wide = sizeof(typename Traits<DT>::U) == 8;
+  static constexpr int value = R == 32 ? MF_MINB_R32 : R == 16 ? MF_MINB_R16 : R == 8 ? MF_MINB_R8
+                               : R == 4 ? (wide ? MF_MINB_R4_WIDE : MF_MINB_R4) : 0;
 };
 
 // src[] holds one u16 entry per merged position q, in position order with two pad entries
@@ -165,7 +171,7 @@ __device__ __forceinline__ uint32_t src_slot(uint32_t q) {
 template <int R> struct MergeChains { static constexpr int value = R == 32 ? MF_MERGE_NC32 : R == 8 ? MF_MERGE_NC8 : 1; };
 
 template <int DT, int R, int W, int WP>
-__global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<R>::value) mf_medium_kernel(Geom g, uint64_t tiles_per_row, uint64_t total_tiles) {
+__global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<DT, R>::value) mf_medium_kernel(Geom g, uint64_t tiles_per_row, uint64_t total_tiles) {
   using C = MediumCfg<DT, R, W, WP>;
   using Tr = typename C::Tr;
   using U = typename C::U;
