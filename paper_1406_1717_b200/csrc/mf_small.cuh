@@ -18,7 +18,8 @@
 //
 // Persistent CTAs stream tiles of T consecutive units: while a tile is sorted and
 // walked, the next tile's T+1 blocks are already in flight into the other half of a
-// double buffer (cp.async, 16-byte chunks), so HBM reads overlap the compute.  The
+// double buffer (one TMA bulk copy per tile, completing on an mbarrier), so HBM reads
+// overlap the compute.  The
 // sorted keys and ranks use a lane-interleaved [position][column] layout whose column
 // stride is a multiple of 32, so every warp access is conflict-free regardless of
 // the data-dependent cursor positions.
