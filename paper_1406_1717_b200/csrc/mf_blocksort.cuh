@@ -64,7 +64,10 @@ __device__ __forceinline__ void merge_levels_s(E* s, int b0, int tid, int run0, 
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       // branch-free step: one shared load refills whichever side was consumed
-      const bool takeA = (ib >= run) || (ia < run && E::less(xa, yv));
+      // 8-byte elements (32-bit keys): bitwise, so no branch per step (c5 50.7 -> 49.0 ms); with 64-bit
+      // keys the short-circuit form measured faster (c1 0.0466 against 0.0498 ms)
+      const bool takeA = sizeof(E) == 8 ? (bool)((ib >= run) | ((ia < run) & E::less(xa, yv)))
+                                        : (ib >= run) || (ia < run && E::less(xa, yv));
       v[r] = E::select(takeA, xa, yv);
       ia += takeA;
       ib += !takeA;
@@ -432,7 +435,7 @@ __device__ __forceinline__ void team_sort_keys(KElem32* sb, const typename Trait
     uint32_t o[RS];
 #pragma unroll
     for (int r = 0; r < RS; ++r) {
-      const bool takeA = (ib >= NS) || (ia < NS && xa <= yb);
+      const bool takeA = (ib >= NS) | ((ia < NS) & (xa <= yb));
       o[r] = takeA ? xa : yb;
       ia += takeA;
       ib += !takeA;

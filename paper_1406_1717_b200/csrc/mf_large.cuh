@@ -448,7 +448,8 @@ __device__ __forceinline__ int merge_tile(E* s, const E* X, const E* Y, uint32_t
     cnt = min(LR2, tot - dd);
 #pragma unroll
     for (int r = 0; r < LR2; ++r) {
-      const bool takeA = (ib >= NY) || (ia < NX && before(xa, yv));
+      const bool takeA = sizeof(E) == 8 ? (bool)((ib >= NY) | ((ia < NX) & before(xa, yv)))  // no branch per step
+                                        : (ib >= NY) || (ia < NX && before(xa, yv));
       v[r] = E::select(takeA, xa, yv);
       srcB[r] = !takeA;
       ia += takeA;
