@@ -25,6 +25,9 @@ cudaError_t launch_k(const Geom& g, cudaStream_t s) { return small_launch_k<DT, 
 #define MF_MED3 1  // 0: k = 3 runs the generic small kernel
 #endif
 constexpr int kMed3Threads = 256;
+#ifndef MF_MED3_CS
+#define MF_MED3_CS 0  // 1: ld.global.cs / st.global.cs (streaming) for the vector loads and stores
+#endif
 #ifndef MF_MED3_Q
 #define MF_MED3_Q 2  // 16-byte loads per thread and chunk (a warp's loads are contiguous)
 #endif
@@ -85,7 +88,13 @@ __global__ void __launch_bounds__(kMed3Threads) mf_med3_kernel(Geom g, uint64_t 
       if (vec && wb + WSPAN <= g.keep) {                           // then wb + WSPAN + 2 <= n
         uint4 q[Q];
 #pragma unroll
-        for (int j = 0; j < Q; ++j) q[j] = __ldg(reinterpret_cast<const uint4*>(x + wb) + j * 32 + lane);
+        for (int j = 0; j < Q; ++j) {
+#if MF_MED3_CS
+          q[j] = __ldcs(reinterpret_cast<const uint4*>(x + wb) + j * 32 + lane);   // streamed once: evict first
+#else
+          q[j] = __ldg(reinterpret_cast<const uint4*>(x + wb) + j * 32 + lane);
+#endif
+        }
         T h0 = T(0), h1 = T(0);                                    // the two samples past the warp's run
         if (lane == 0) { h0 = __ldg(x + wb + WSPAN); h1 = __ldg(x + wb + WSPAN + 1); }
 #pragma unroll
@@ -112,7 +121,11 @@ __global__ void __launch_bounds__(kMed3Threads) mf_med3_kernel(Geom g, uint64_t 
           for (int i = 0; i < E4; ++i) out[i] = K::g(med3<U>(kk[i], kk[i + 1], kk[i + 2]));
           uint4 o;
           memcpy(&o, &out[0], 16);
+#if MF_MED3_CS
+          __stcs(reinterpret_cast<uint4*>(y + wb) + j * 32 + lane, o);
+#else
           reinterpret_cast<uint4*>(y + wb)[j * 32 + lane] = o;
+#endif
         }
       } else {                                                     // ragged tail or unaligned rows
         for (uint64_t o = wb + lane; o < min(wb + WSPAN, g.keep); o += 32)
