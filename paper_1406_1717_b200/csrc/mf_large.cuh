@@ -831,14 +831,38 @@ __global__ void __launch_bounds__(LNT) ml_walk(LargeGeom L, const typename Trait
     win = (uint64_t)cb | ((uint64_t)word(cw + 1, i0) << 32);
   }
   const uint32_t my_n = active ? i1 - i0 : 0u;
+  // Steps run in groups of 8.  The group's Delete/Undelete targets (rab) are loaded one group
+  // ahead, and its 8 median keys are gathered into registers and staged after the group, so a
+  // thread has up to 16 independent loads in flight instead of stalling on each step's two
+  // (the kernel was bound by long-scoreboard stalls: 14 per issued instruction).
+#ifndef MF_WALK_PREFETCH
+#define MF_WALK_PREFETCH 1
+#endif
+  auto load_group = [&](uint32_t t0, uint2 (&ab)[8]) {
+#pragma unroll
+    for (uint32_t tt = 0; tt < 8; ++tt) {
+      const uint32_t t = t0 + tt;
+      ab[tt] = (t > 0 && t < my_n) ? __ldg(rb + (uint64_t)(t - 1) * L.C) : make_uint2(0u, 0u);
+    }
+  };
+  uint2 abn[8];
+  if (MF_WALK_PREFETCH) load_group(0, abn);
   for (uint32_t t0 = 0; t0 < L.CL; t0 += 8) {
-#pragma unroll 2
+    uint2 abc[8];
+    U kv[8];
+    if (MF_WALK_PREFETCH) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) abc[j] = abn[j];
+      if (t0 + 8 < L.CL) load_group(t0 + 8, abn);
+    }
+#pragma unroll
     for (uint32_t tt = 0; tt < 8; ++tt) {
       const uint32_t t = t0 + tt;
       const uint32_t i = i0 + t;
+      kv[tt] = 0;
       if (t < my_n) {
         if (t > 0) {
-          const uint2 ab = __ldg(rb + (uint64_t)(t - 1) * L.C);
+          const uint2 ab = MF_WALK_PREFETCH ? abc[tt] : __ldg(rb + (uint64_t)(t - 1) * L.C);
           const uint32_t a = ab.x, b = ab.y;
           MF_ASSERT(a < L.nq && b < L.nq);
           const uint32_t base = cw0 * 32;
@@ -864,9 +888,11 @@ __global__ void __launch_bounds__(LNT) ml_walk(LargeGeom L, const typename Trait
           p = sel(up, cw0 * 32 + __ffsll((long long)m) - 1, sel(down, cw0 * 32 + 63 - __clzll((long long)m), p));
         }
         MF_ASSERT(p < L.nq);
-        stage[lane * 9 + tt] = __ldg(mkg + p);
+        kv[tt] = __ldg(mkg + p);
       }
     }
+#pragma unroll
+    for (uint32_t tt = 0; tt < 8; ++tt) stage[lane * 9 + tt] = kv[tt];
     __syncwarp();
     // 8 outputs of 4 chunks per warp store: lane l -> chunk 4j + l/8, step l%8
 #pragma unroll
