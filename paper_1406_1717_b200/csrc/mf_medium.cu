@@ -36,7 +36,14 @@ template <int DT, int R> struct WarpsFor {
 template <int DT, int R>
 cudaError_t launch_r(const Geom& g, cudaStream_t s) {
   constexpr int W = WarpsFor<DT, R>::value;
-  constexpr int WP = R >= 32 ? 2 : 1;  // warps per block pair (team); k <= 511 measured faster with 1
+#ifndef MF_WP_R16
+#define MF_WP_R16 1
+#endif
+#ifndef MF_WP_R8
+#define MF_WP_R8 1
+#endif
+  // warps per block pair (team); k <= 511 measured faster with 1
+  constexpr int WP = R >= 32 ? 2 : R == 16 ? MF_WP_R16 : R == 8 ? MF_WP_R8 : 1;
   using C = MediumCfg<DT, R, W, WP>;
   auto kern = mf_medium_kernel<DT, R, W, WP>;
   LaunchInfo li;
