@@ -333,8 +333,13 @@ __global__ void __launch_bounds__(32 * W * WP, MediumMinBlocks<DT, R>::value) mf
     const TV* __restrict__ x = reinterpret_cast<const TV*>(g.x) + row * g.ld_x;
     TV* __restrict__ y = reinterpret_cast<TV*>(g.y) + row * g.ld_y;
     const bool carry = (row == prev_row && tr == prev_tile + 1);
-    if (carry) base = (base + W) % (W + 1);
-    auto slot = [&](uint32_t logical) { return ring + ((base + logical) % (W + 1)) * SLOT; };
+    // ring arithmetic with one conditional subtract (base and logical are <= W)
+    if (carry) { base += W; base -= base > (uint32_t)W ? W + 1 : 0; }
+    auto slot = [&](uint32_t logical) {
+      uint32_t b = base + logical;
+      b -= b > (uint32_t)W ? W + 1 : 0;
+      return ring + b * SLOT;
+    };
 
     // ---------------- phase 1: team block sorts ----------------
     if (!carry && team == 0) {
